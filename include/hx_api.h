@@ -1,0 +1,142 @@
+/*
+ * hx_api.h -- C-ABI of the B200 (sm_100a) asymmetric TP/PP decoder data path.
+ *
+ * The reference (heteroplan, pure Python) has no FFI: its runtime boundary is
+ * the plan document (reference pkg/src/heteroplan/cli.py:75-115) plus the
+ * per-(replica, task) service-time table (pkg/src/heteroplan/simulate.py:135-142),
+ * and the paper's per-layer math is what these entry points
+ * execute. Each function below replaces one term of the reference's closed-form
+ * stand-in for the path (pkg/src/heteroplan/costs.py:106-176):
+ *
+ *   hx_linear                 weight-scan + FLOP terms   costs.py:114-119
+ *   hx_rope_kv_append,
+ *   hx_attn_decode_paged,
+ *   hx_attn_prefill           attention / KV concat
+ *   hx_residual_add_rmsnorm   "+ x" residual after each all-reduce
+ *   hx_argmax_*               greedy token selection (not modelled by the reference)
+ *   hx_kv_bytes               KV part of mem_footprint   costs.py:168-176
+ *
+ * Conventions (no torch types cross this boundary):
+ *   - every pointer is a device pointer owned by the caller; the library never
+ *     allocates or frees; scratch is passed in as (workspace, bytes);
+ *   - every call is asynchronous on `stream` (a cudaStream_t) and returns 0 on
+ *     success or a positive hx error code / cudaError_t value (hx_error_string);
+ *   - dtype codes: HX_F32 (fp32 mode) or HX_BF16 (bf16 mode); accumulation and
+ *     softmax are always fp32; the residual stream `x` is always fp32;
+ *   - matrices are row-major; weights are [out, in] (nn.Linear layout), so
+ *     Y[t, n] = sum_k X[t, k] * W[n, k];
+ *   - paged KV layout: cache[block][kv_head][page_size][head_dim] (K and V in
+ *     separate arrays), block_table[seq][max_blocks] (int32 block ids),
+ *     seq_lens[seq] = tokens already cached before this call (int32).
+ */
+#ifndef HX_API_H
+#define HX_API_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void *hx_stream_t; /* cudaStream_t */
+
+enum hx_dtype { HX_F32 = 0, HX_BF16 = 1 };
+
+enum hx_status {
+  HX_OK = 0,
+  HX_ERR_ARG = 1001,        /* bad shape / pointer / dtype combination */
+  HX_ERR_UNSUPPORTED = 1002, /* shape the kernels do not implement */
+  HX_ERR_WORKSPACE = 1003,   /* workspace too small */
+  HX_ERR_DRIVER = 1004       /* cuTensorMapEncodeTiled unavailable / failed */
+};
+
+/* library identity, error text, and a count of kernels launched so far */
+int hx_version(void);
+const char *hx_error_string(int code);
+uint64_t hx_launch_count(void);
+
+/* x[t, :] = float(table[ids[t], :]);  table [vocab, hidden] (dtype) */
+int hx_embed(const int32_t *ids, const void *table, int table_dtype, float *x,
+             int n_tok, int hidden, int vocab, hx_stream_t stream);
+
+/* out[t, :] = x[t * ldx, :] / sqrt(mean(x^2) + eps) * gain  (out in out_dtype,
+ * rows contiguous). ldx = row pitch of x in elements (>= hidden), which lets
+ * the last stage normalise only each sequence's last prompt token. */
+int hx_rmsnorm(const float *x, int ldx, const float *gain, void *out, int out_dtype,
+               int n_tok, int hidden, float eps, hx_stream_t stream);
+
+/* x += delta (fp32, the all-reduced row-parallel output); out = rmsnorm(x)*gain.
+ * out may be NULL (residual add only). */
+int hx_residual_add_rmsnorm(float *x, const float *delta, const float *gain,
+                            void *out, int out_dtype, int n_tok, int hidden,
+                            float eps, hx_stream_t stream);
+
+/* Y[t, n] (+)= sum_k X[t, k] W[n, k], t < n_tok, n < n_out, k < k_dim.
+ * bf16 weights+activations: tcgen05/TMEM tensor-core kernel fed by TMA
+ * (split-K for decode-sized n_tok, fp32 accumulate); fp32: CUDA-core kernel.
+ * y_dtype HX_F32 or HX_BF16; ldy = row pitch of Y in elements; flags bit0:
+ * accumulate into Y (fp32 Y only). workspace >= hx_linear_workspace(...). */
+int hx_linear(const void *w, const void *x, void *y, int dtype, int y_dtype,
+              int n_tok, int n_out, int k_dim, int ldy, int flags,
+              void *workspace, size_t workspace_bytes, hx_stream_t stream);
+size_t hx_linear_workspace(int dtype, int n_tok, int n_out, int k_dim);
+
+/* out[t, j] = silu(gu[t, j]) * gu[t, inter + j], j < inter */
+int hx_swiglu(const void *gu, void *out, int dtype, int n_tok, int inter,
+              hx_stream_t stream);
+
+/* RoPE (rotate-half, theta) on q and k of the packed qkv rows
+ * [n_tok, (hq + 2 hkv) * hd], write roped q to q_out [n_tok, hq, hd] and k, v
+ * into the paged cache. Decode (prefill_len == 0): token t is seq t at
+ * position seq_lens[t]. Prefill (prefill_len = s): token t is seq t / s at
+ * position seq_lens[t / s] + t % s. */
+int hx_rope_kv_append(const void *qkv, void *q_out, void *k_cache, void *v_cache,
+                      const int32_t *block_table, const int32_t *seq_lens,
+                      int dtype, int n_tok, int prefill_len, int hq, int hkv,
+                      int hd, int page_size, int max_blocks, float theta,
+                      hx_stream_t stream);
+
+/* Decode attention over the paged cache for one new token per sequence:
+ * o[b, h, :] = softmax(q[b, h] . K[b, h/g]^T / sqrt(hd)) V, context length
+ * seq_lens[b] + 1 (the token appended by hx_rope_kv_append). Split-KV with an
+ * in-kernel combine; workspace >= hx_attn_decode_workspace(...). */
+int hx_attn_decode_paged(const void *q, const void *k_cache, const void *v_cache,
+                         const int32_t *block_table, const int32_t *seq_lens,
+                         void *o, int dtype, int batch, int hq, int hkv, int hd,
+                         int page_size, int max_blocks, int max_ctx,
+                         void *workspace, size_t workspace_bytes,
+                         hx_stream_t stream);
+size_t hx_attn_decode_workspace(int batch, int hq, int hkv, int hd, int max_ctx);
+
+/* Causal prefill attention: q [batch*s, hq, hd] (roped), keys/values are the
+ * s prompt tokens already appended to the paged cache (positions
+ * seq_lens[b] .. seq_lens[b]+s-1, with seq_lens the values BEFORE append). */
+int hx_attn_prefill(const void *q, const void *k_cache, const void *v_cache,
+                    const int32_t *block_table, const int32_t *seq_lens,
+                    void *o, int dtype, int batch, int s, int hq, int hkv,
+                    int hd, int page_size, int max_blocks, hx_stream_t stream);
+
+/* seq_lens[b] += n for b < batch (end of a stage step). */
+int hx_advance(int32_t *seq_lens, int batch, int n, hx_stream_t stream);
+
+/* Greedy selection, vocab-parallel: key[t] = pack(max_j logits[t, j],
+ * smallest argmax j + vocab_offset) as an int64 whose signed order is
+ * (value, -index); MAX-reducing keys across TP ranks gives the global argmax
+ * with torch.argmax tie-breaking (first index). */
+int hx_argmax_partial(const float *logits, int64_t *keys, int n_tok, int n_cols,
+                      int ld, int vocab_offset, hx_stream_t stream);
+
+/* ids[t] = unpack(key[t]); if history != NULL also history[t * s_out + *step]
+ * = ids[t] and, when bump_step != 0, ++*step (one thread, after all writes). */
+int hx_argmax_finalize(const int64_t *keys, int32_t *ids, int32_t *history,
+                       int32_t *step, int s_out, int n_tok, int bump_step,
+                       hx_stream_t stream);
+
+/* KV bytes one rank holds for `layers` layers (part of mem_footprint). */
+size_t hx_kv_bytes(int dtype, int layers, int num_blocks, int hkv_rank, int page_size, int hd);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HX_API_H */

@@ -1,0 +1,448 @@
+// Attention and the paged KV cache: RoPE + KV append,
+// split-KV decode attention over pages with an in-kernel combine, and causal
+// prefill attention. The decode kernel is HBM-bound on the KV read (8-15% of
+// the decode step's bytes); the prefill kernel is a tiled
+// flash-style CUDA-core kernel (attention is ~1-6% of prefill FLOPs).
+//
+// Paged layout: cache[block][kv_head][page][hd]; token position p of seq b
+// lives in block block_table[b * max_blocks + p / page] at slot p % page.
+#include "hx_common.cuh"
+
+namespace hx {
+
+__device__ __forceinline__ size_t page_index(const int32_t *bt, int b, int pos, int max_blocks, int page,
+                                             int hkv, int kvh, int hd) {
+  const int blk = bt[(size_t)b * max_blocks + pos / page];
+  return (((size_t)blk * hkv + kvh) * page + pos % page) * hd;
+}
+
+// ------------------------------------------------------------- RoPE + append
+template <typename T>
+__global__ void rope_append_kernel(const T *qkv, T *q_out, T *kc, T *vc, const int32_t *bt,
+                                   const int32_t *seq_lens, int prefill_len, int hq, int hkv, int hd,
+                                   int page, int max_blocks, float theta) {
+  const int t = blockIdx.x;
+  const int b = prefill_len ? t / prefill_len : t;
+  const int pos = seq_lens[b] + (prefill_len ? t % prefill_len : 0);
+  const int half = hd / 2;
+  const int row = (hq + 2 * hkv) * hd;
+  const T *src = qkv + (size_t)t * row;
+  const int n_rope = (hq + hkv) * half;
+  for (int w = threadIdx.x; w < n_rope + hkv * hd; w += blockDim.x) {
+    if (w < n_rope) {
+      const int h = w / half, i = w % half;
+      const float inv_freq = 1.0f / powf(theta, (float)(2 * i) / (float)hd);
+      const float ang = (float)pos * inv_freq;
+      float s, c;
+      sincosf(ang, &s, &c);
+      const float x1 = to_f32(src[h * hd + i]);
+      const float x2 = to_f32(src[h * hd + i + half]);
+      const float y1 = x1 * c - x2 * s;  // x * cos + rotate_half(x) * sin
+      const float y2 = x2 * c + x1 * s;
+      if (h < hq) {
+        T *dst = q_out + ((size_t)t * hq + h) * hd;
+        dst[i] = from_f32<T>(y1);
+        dst[i + half] = from_f32<T>(y2);
+      } else {
+        T *dst = kc + page_index(bt, b, pos, max_blocks, page, hkv, h - hq, hd);
+        dst[i] = from_f32<T>(y1);
+        dst[i + half] = from_f32<T>(y2);
+      }
+    } else {
+      const int v = w - n_rope;
+      const int h = v / hd, d = v % hd;
+      vc[page_index(bt, b, pos, max_blocks, page, hkv, h, hd) + d] = src[(hq + hkv) * hd + v];
+    }
+  }
+}
+
+// ------------------------------------------------------------- decode
+// CTA = (seq b, kv head, split); 4 warps; a "lane group" of LG = HD / V lanes
+// owns one token at a time (V = elements per 16-byte load), so a warp works on
+// 32 / LG tokens concurrently and every lane issues U independent K and V
+// 16-byte loads per iteration.
+constexpr int DEC_THREADS = 128;
+
+template <typename T, int HD, int G>
+__global__ void __launch_bounds__(DEC_THREADS)
+    attn_decode_kernel(const T *q, const T *kc, const T *vc, const int32_t *bt, const int32_t *seq_lens,
+                       T *o, int hkv, int page, int max_blocks, float scale, float *ws, int *counters) {
+  constexpr int V = Vec16<T>::N;
+  constexpr int LG = HD / V;
+  constexpr int GPW = 32 / LG;
+  constexpr int NG = (DEC_THREADS / 32) * GPW;
+  constexpr int U = 4;
+  const int b = blockIdx.x / hkv, kvh = blockIdx.x % hkv;
+  const int split = blockIdx.y, splits = gridDim.y;
+  const int hq = hkv * G;
+  const int ctx = seq_lens[b] + 1;
+  const int chunk = (ctx + splits - 1) / splits;
+  const int t0 = split * chunk, t1 = min(ctx, t0 + chunk);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int grp = warp * GPW + lane / LG, gl = lane % LG;
+  const int d0 = gl * V;
+
+  float qv[G][V];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    Vec16<T>::load(q + ((size_t)b * hq + kvh * G + g) * HD + d0, qv[g]);
+#pragma unroll
+    for (int j = 0; j < V; ++j) qv[g][j] *= scale;
+  }
+  float m[G], l[G], acc[G][V];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    m[g] = -INFINITY;
+    l[g] = 0.f;
+#pragma unroll
+    for (int j = 0; j < V; ++j) acc[g][j] = 0.f;
+  }
+  const int32_t *btb = bt + (size_t)b * max_blocks;
+  for (int base = t0; base < t1; base += NG * U) {  // warp-uniform trip count (shuffles below)
+    float kv[U][V], vv[U][V];
+    bool ok[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int p = base + u * NG + grp;
+      ok[u] = p < t1;
+      if (ok[u]) {
+        const size_t off = (((size_t)btb[p / page] * hkv + kvh) * page + p % page) * HD + d0;
+        Vec16<T>::load(kc + off, kv[u]);
+        Vec16<T>::load(vc + off, vv[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float s[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        float a = 0.f;
+#pragma unroll
+        for (int j = 0; j < V; ++j) a = fmaf(qv[g][j], kv[u][j], a);
+#pragma unroll
+        for (int off = LG / 2; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+        s[g] = a;
+      }
+      if (!ok[u]) continue;
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const float mn = fmaxf(m[g], s[g]);
+        const float corr = __expf(m[g] - mn);
+        const float pr = __expf(s[g] - mn);
+        l[g] = l[g] * corr + pr;
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc[g][j] = fmaf(pr, vv[u][j], acc[g][j] * corr);
+        m[g] = mn;
+      }
+    }
+  }
+
+  // combine the NG lane groups of this CTA
+  __shared__ float sm_m[NG][G], sm_l[NG][G];
+  __shared__ float sm_acc[NG][G][HD];
+  if (gl == 0) {
+#pragma unroll
+    for (int g = 0; g < G; ++g) { sm_m[grp][g] = m[g]; sm_l[grp][g] = l[g]; }
+  }
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+#pragma unroll
+    for (int j = 0; j < V; ++j) sm_acc[grp][g][d0 + j] = acc[g][j];
+  __syncthreads();
+  // per (g, d): merge groups -> (M, L, A) for this split
+  const size_t pair = (size_t)b * hkv + kvh;
+  for (int w = threadIdx.x; w < G * HD; w += DEC_THREADS) {
+    const int g = w / HD, d = w % HD;
+    float M = -INFINITY;
+    for (int i = 0; i < NG; ++i) M = fmaxf(M, sm_m[i][g]);
+    float L = 0.f, A = 0.f;
+    if (M != -INFINITY) {
+      for (int i = 0; i < NG; ++i) {
+        const float c = __expf(sm_m[i][g] - M);
+        L += sm_l[i][g] * c;
+        A += sm_acc[i][g][d] * c;
+      }
+    }
+    if (splits == 1) {
+      o[((size_t)b * hq + kvh * G + g) * HD + d] = from_f32<T>(A / L);
+    } else {
+      float *part = ws + ((pair * splits + split) * G + g) * (HD + 2);
+      part[d] = A;
+      if (d == 0) { part[HD] = M; part[HD + 1] = L; }
+    }
+  }
+  if (splits == 1) return;
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int tk = atomicAdd(&counters[pair], 1);
+    s_last = tk == splits - 1;
+    if (s_last) counters[pair] = 0;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int w = threadIdx.x; w < G * HD; w += DEC_THREADS) {
+    const int g = w / HD, d = w % HD;
+    float M = -INFINITY;
+    for (int s = 0; s < splits; ++s) M = fmaxf(M, __ldcg(ws + ((pair * splits + s) * G + g) * (HD + 2) + HD));
+    float L = 0.f, A = 0.f;
+    for (int s = 0; s < splits; ++s) {
+      const float *part = ws + ((pair * splits + s) * G + g) * (HD + 2);
+      const float ms = __ldcg(part + HD);
+      if (ms == -INFINITY) continue;
+      const float c = __expf(ms - M);
+      L += __ldcg(part + HD + 1) * c;
+      A += __ldcg(part + d) * c;
+    }
+    o[((size_t)b * hq + kvh * G + g) * HD + d] = from_f32<T>(A / L);
+  }
+}
+
+// ------------------------------------------------------------- prefill
+// CTA = (64 queries, q head, seq); 256 threads; fp32 smem tiles; online softmax.
+constexpr int PF_BQ = 64, PF_BK = 64, PF_THREADS = 256;
+
+template <typename T, int HD>
+__global__ void __launch_bounds__(PF_THREADS)
+    attn_prefill_kernel(const T *q, const T *kc, const T *vc, const int32_t *bt, const int32_t *seq_lens,
+                        T *o, int s_len, int hq, int hkv, int page, int max_blocks, float scale) {
+  extern __shared__ float sm[];
+  float *Qs = sm;                         // [BQ][HD]
+  float *Ks = Qs + PF_BQ * HD;            // [BK][HD + 1]
+  float *Vs = Ks + PF_BK * (HD + 1);      // [BK][HD]
+  float *Ps = Vs + PF_BK * HD;            // [BQ][BK + 1]
+  const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int kvh = h / (hq / hkv);
+  const int p0 = seq_lens[b];
+  const int q0 = qt * PF_BQ;
+  const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+  constexpr int DPT = HD / 16;  // output dims per thread
+  for (int i = tid; i < PF_BQ * HD; i += PF_THREADS) {
+    const int r = i / HD, d = i % HD;
+    const int qi = q0 + r;
+    Qs[i] = qi < s_len ? to_f32(q[(((size_t)b * s_len + qi) * hq + h) * HD + d]) * scale : 0.f;
+  }
+  float m[4], l[4], acc[4][DPT];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    m[i] = -INFINITY;
+    l[i] = 0.f;
+#pragma unroll
+    for (int j = 0; j < DPT; ++j) acc[i][j] = 0.f;
+  }
+  const int q_last = min(s_len, q0 + PF_BQ) - 1;
+  for (int k0 = 0; k0 <= q_last; k0 += PF_BK) {
+    __syncthreads();
+    for (int i = tid; i < PF_BK * HD; i += PF_THREADS) {
+      const int r = i / HD, d = i % HD;
+      const int kj = k0 + r;
+      float kvk = 0.f, kvv = 0.f;
+      if (kj < s_len) {
+        const size_t off = page_index(bt, b, p0 + kj, max_blocks, page, hkv, kvh, HD) + d;
+        kvk = to_f32(kc[off]);
+        kvv = to_f32(vc[off]);
+      }
+      Ks[r * (HD + 1) + d] = kvk;
+      Vs[r * HD + d] = kvv;
+    }
+    __syncthreads();
+    // S = Q K^T for rows ty*4+i, cols tx*4+j
+    float s[4][4] = {};
+    for (int d = 0; d < HD; ++d) {
+      float a[4], kk[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = Qs[(ty * 4 + i) * HD + d];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) kk[j] = Ks[(tx * 4 + j) * (HD + 1) + d];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) s[i][j] = fmaf(a[i], kk[j], s[i][j]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int qi = q0 + ty * 4 + i;
+      float rmax = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int kj = k0 + tx * 4 + j;
+        if (kj > qi || kj >= s_len) s[i][j] = -INFINITY;
+        rmax = fmaxf(rmax, s[i][j]);
+      }
+#pragma unroll
+      for (int off = 8; off > 0; off >>= 1) rmax = fmaxf(rmax, __shfl_xor_sync(0xffffffffu, rmax, off));
+      const float mn = fmaxf(m[i], rmax);
+      const float corr = mn == -INFINITY ? 1.f : __expf(m[i] - mn);
+      float rs = 0.f;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float pr = mn == -INFINITY ? 0.f : __expf(s[i][j] - mn);
+        Ps[(ty * 4 + i) * (PF_BK + 1) + tx * 4 + j] = pr;
+        rs += pr;
+      }
+#pragma unroll
+      for (int off = 8; off > 0; off >>= 1) rs += __shfl_xor_sync(0xffffffffu, rs, off);
+      l[i] = l[i] * corr + rs;
+      m[i] = mn;
+#pragma unroll
+      for (int j = 0; j < DPT; ++j) acc[i][j] *= corr;
+    }
+    __syncthreads();
+    for (int c = 0; c < PF_BK; ++c) {
+      float vv[DPT];
+#pragma unroll
+      for (int j = 0; j < DPT; ++j) vv[j] = Vs[c * HD + tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float pr = Ps[(ty * 4 + i) * (PF_BK + 1) + c];
+#pragma unroll
+        for (int j = 0; j < DPT; ++j) acc[i][j] = fmaf(pr, vv[j], acc[i][j]);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int qi = q0 + ty * 4 + i;
+    if (qi >= s_len) continue;
+    T *dst = o + (((size_t)b * s_len + qi) * hq + h) * HD;
+#pragma unroll
+    for (int j = 0; j < DPT; ++j) dst[tx + 16 * j] = from_f32<T>(acc[i][j] / l[i]);
+  }
+}
+
+static int decode_splits(int batch, int hkv, int max_ctx) {
+  const int pairs = batch * hkv;
+  const int target = 2 * 148;
+  int s = (target + pairs - 1) / pairs;
+  const int cap = (max_ctx + 127) / 128;
+  s = s < cap ? s : cap;
+  return s < 1 ? 1 : s;
+}
+
+template <typename T, int HD>
+static int launch_decode_g(int G, dim3 grid, const void *q, const void *kc, const void *vc, const int32_t *bt,
+                           const int32_t *sl, void *o, int hkv, int page, int maxb, float scale, float *ws,
+                           int *cnt, cudaStream_t st) {
+#define HX_DEC(GG)                                                                                      \
+  attn_decode_kernel<T, HD, GG><<<grid, DEC_THREADS, 0, st>>>((const T *)q, (const T *)kc, (const T *)vc, bt, \
+                                                              sl, (T *)o, hkv, page, maxb, scale, ws, cnt)
+  switch (G) {
+    case 1: HX_DEC(1); break;
+    case 2: HX_DEC(2); break;
+    case 4: HX_DEC(4); break;
+    case 8: HX_DEC(8); break;
+    default: return HX_ERR_UNSUPPORTED;
+  }
+#undef HX_DEC
+  return launch_status();
+}
+
+}  // namespace hx
+
+using namespace hx;
+
+extern "C" int hx_rope_kv_append(const void *qkv, void *q_out, void *k_cache, void *v_cache,
+                                 const int32_t *block_table, const int32_t *seq_lens, int dtype, int n_tok,
+                                 int prefill_len, int hq, int hkv, int hd, int page_size, int max_blocks,
+                                 float theta, hx_stream_t stream) {
+  if (n_tok == 0) return 0;
+  if (!qkv || !q_out || !k_cache || !v_cache || !block_table || !seq_lens || hd % 2 || page_size <= 0)
+    return HX_ERR_ARG;
+  cudaStream_t st = as_stream(stream);
+  if (dtype == HX_BF16)
+    rope_append_kernel<<<n_tok, 256, 0, st>>>((const __nv_bfloat16 *)qkv, (__nv_bfloat16 *)q_out,
+                                              (__nv_bfloat16 *)k_cache, (__nv_bfloat16 *)v_cache, block_table,
+                                              seq_lens, prefill_len, hq, hkv, hd, page_size, max_blocks, theta);
+  else
+    rope_append_kernel<<<n_tok, 256, 0, st>>>((const float *)qkv, (float *)q_out, (float *)k_cache,
+                                              (float *)v_cache, block_table, seq_lens, prefill_len, hq, hkv, hd,
+                                              page_size, max_blocks, theta);
+  return launch_status();
+}
+
+extern "C" size_t hx_attn_decode_workspace(int batch, int hq, int hkv, int hd, int max_ctx) {
+  const int s = decode_splits(batch, hkv, max_ctx);
+  if (s <= 1) return 0;
+  const size_t counters = ((size_t)batch * hkv * sizeof(int) + 255) & ~size_t(255);
+  return counters + (size_t)batch * hkv * s * (hq / hkv) * (hd + 2) * sizeof(float);
+}
+
+extern "C" int hx_attn_decode_paged(const void *q, const void *k_cache, const void *v_cache,
+                                    const int32_t *block_table, const int32_t *seq_lens, void *o, int dtype,
+                                    int batch, int hq, int hkv, int hd, int page_size, int max_blocks,
+                                    int max_ctx, void *workspace, size_t workspace_bytes, hx_stream_t stream) {
+  if (batch == 0) return 0;
+  if (!q || !k_cache || !v_cache || !block_table || !seq_lens || !o || hq % hkv) return HX_ERR_ARG;
+  const int G = hq / hkv;
+  const int splits = decode_splits(batch, hkv, max_ctx);
+  float *ws = nullptr;
+  int *cnt = nullptr;
+  if (splits > 1) {
+    if (!workspace || workspace_bytes < hx_attn_decode_workspace(batch, hq, hkv, hd, max_ctx))
+      return HX_ERR_WORKSPACE;
+    const size_t counters = ((size_t)batch * hkv * sizeof(int) + 255) & ~size_t(255);
+    cnt = reinterpret_cast<int *>(workspace);
+    ws = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(workspace) + counters);
+  }
+  dim3 grid(batch * hkv, splits);
+  const float scale = 1.0f / sqrtf((float)hd);
+  cudaStream_t st = as_stream(stream);
+#define HX_ARGS grid, q, k_cache, v_cache, block_table, seq_lens, o, hkv, page_size, max_blocks, scale, ws, cnt, st
+  if (dtype == HX_BF16) {
+    switch (hd) {
+      case 32: return launch_decode_g<__nv_bfloat16, 32>(G, HX_ARGS);
+      case 64: return launch_decode_g<__nv_bfloat16, 64>(G, HX_ARGS);
+      case 128: return launch_decode_g<__nv_bfloat16, 128>(G, HX_ARGS);
+    }
+  } else {
+    switch (hd) {
+      case 32: return launch_decode_g<float, 32>(G, HX_ARGS);
+      case 64: return launch_decode_g<float, 64>(G, HX_ARGS);
+      case 128: return launch_decode_g<float, 128>(G, HX_ARGS);
+    }
+  }
+#undef HX_ARGS
+  return HX_ERR_UNSUPPORTED;
+}
+
+template <typename T, int HD>
+static int launch_prefill(const void *q, const void *kc, const void *vc, const int32_t *bt, const int32_t *sl,
+                          void *o, int batch, int s, int hq, int hkv, int page, int maxb, cudaStream_t st) {
+  const size_t smem = sizeof(float) * (PF_BQ * HD + PF_BK * (HD + 1) + PF_BK * HD + PF_BQ * (PF_BK + 1));
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_prefill_kernel<T, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  dim3 grid((s + PF_BQ - 1) / PF_BQ, hq, batch);
+  attn_prefill_kernel<T, HD><<<grid, PF_THREADS, smem, st>>>((const T *)q, (const T *)kc, (const T *)vc, bt, sl,
+                                                             (T *)o, s, hq, hkv, page, maxb,
+                                                             1.0f / sqrtf((float)HD));
+  return launch_status();
+}
+
+extern "C" int hx_attn_prefill(const void *q, const void *k_cache, const void *v_cache, const int32_t *block_table,
+                               const int32_t *seq_lens, void *o, int dtype, int batch, int s, int hq, int hkv,
+                               int hd, int page_size, int max_blocks, hx_stream_t stream) {
+  if (batch == 0 || s == 0) return 0;
+  if (!q || !k_cache || !v_cache || !block_table || !seq_lens || !o || hq % hkv) return HX_ERR_ARG;
+  cudaStream_t st = as_stream(stream);
+#define HX_PF(T, D) return launch_prefill<T, D>(q, k_cache, v_cache, block_table, seq_lens, o, batch, s, hq, hkv, page_size, max_blocks, st)
+  if (dtype == HX_BF16) {
+    switch (hd) {
+      case 32: HX_PF(__nv_bfloat16, 32);
+      case 64: HX_PF(__nv_bfloat16, 64);
+      case 128: HX_PF(__nv_bfloat16, 128);
+    }
+  } else {
+    switch (hd) {
+      case 32: HX_PF(float, 32);
+      case 64: HX_PF(float, 64);
+      case 128: HX_PF(float, 128);
+    }
+  }
+#undef HX_PF
+  return HX_ERR_UNSUPPORTED;
+}

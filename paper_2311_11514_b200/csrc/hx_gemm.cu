@@ -1,0 +1,398 @@
+// hx_linear: the TP column/row-parallel projections (QKV, O, gate/up, down,
+// lm_head). Replaces the weight-scan and FLOP terms of the reference cost
+// model (pkg/src/heteroplan/costs.py:114-119).
+//
+// bf16: one tcgen05 kernel computes D[M, N] = A[M, K] . B[N, K]^T with both
+// operands K-major, staged by TMA (128B swizzle) through a STAGES-deep
+// mbarrier ring, accumulated in TMEM by one elected thread, and drained by 4
+// epilogue warps (tcgen05.ld 32x32b). The host picks the orientation:
+//   decode  (n_tok <= 64): A = weights (M = out features, 128-row tiles),
+//            B = activations (N = 16/32/64 tokens): a weight-streaming,
+//            HBM-bound kernel, split-K across CTAs so ~2 CTAs/SM stream
+//            disjoint weight slices; the last CTA of a tile (atomic ticket)
+//            reduces the fp32 partials in split order (deterministic).
+//   prefill (n_tok > 64):  A = activations (M = 128 tokens), B = weights
+//            (N = 256 features): tensor-bound, one 128x256 fp32 tile in TMEM.
+// fp32 mode (parity with the CPU oracle) uses a CUDA-core kernel.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <mutex>
+
+#include "hx_common.cuh"
+
+namespace hx {
+
+constexpr int BM = 128;
+constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle row
+constexpr int kNumSMs = 148;
+
+struct GemmArgs {
+  void *c;
+  long ldm, ldn;  // C[m * ldm + n * ldn]
+  int M, N, K;
+  int c_bf16;
+  int accumulate;
+  int kb_total;
+  int kb_per_split;
+  int a_is_weight;
+  float *ws;
+  int *counters;
+};
+
+template <int BN>
+__device__ __forceinline__ void store_chunk(const GemmArgs &p, int m, int n0, const float *v) {
+  if (m >= p.M) return;
+  if (p.c_bf16) {
+    __nv_bfloat16 *c = reinterpret_cast<__nv_bfloat16 *>(p.c);
+    if (p.ldn == 1 && n0 + 16 <= p.N && ((p.ldm * m + n0) & 7) == 0) {
+      Vec16<__nv_bfloat16>::store(c + m * p.ldm + n0, v);
+      Vec16<__nv_bfloat16>::store(c + m * p.ldm + n0 + 8, v + 8);
+      return;
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (n0 + j < p.N) c[m * p.ldm + (long)(n0 + j) * p.ldn] = __float2bfloat16_rn(v[j]);
+  } else {
+    float *c = reinterpret_cast<float *>(p.c);
+    if (p.ldn == 1 && !p.accumulate && n0 + 16 <= p.N && ((p.ldm * m + n0) & 3) == 0) {
+#pragma unroll
+      for (int j = 0; j < 16; j += 4) Vec16<float>::store(c + m * p.ldm + n0 + j, v + j);
+      return;
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      if (n0 + j < p.N) {
+        float *dst = c + m * p.ldm + (long)(n0 + j) * p.ldn;
+        *dst = p.accumulate ? *dst + v[j] : v[j];
+      }
+    }
+  }
+}
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(128, 1)
+    gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tm_a,
+                        const __grid_constant__ CUtensorMap tm_b, GemmArgs p) {
+  constexpr uint32_t A_BYTES = BM * BK * 2;
+  constexpr uint32_t B_BYTES = BN * BK * 2;
+  constexpr uint32_t TMEM_COLS = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *sa = smem;
+  uint8_t *sb = smem + STAGES * A_BYTES;
+  uint64_t *full = reinterpret_cast<uint64_t *>(sb + STAGES * B_BYTES);
+  uint64_t *empty = full + STAGES;
+  uint64_t *accf = empty + STAGES;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(accf + 1);
+  __shared__ int s_last;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const int split = blockIdx.z, splits = gridDim.z;
+  const int kb0 = split * p.kb_per_split;
+  const int kb1 = min(p.kb_total, kb0 + p.kb_per_split);
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tm_a);
+    tma_prefetch(&tm_b);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(accf, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // TMA producer
+    const uint64_t pol_w = l2_policy_evict_first(), pol_x = l2_policy_evict_last();
+    const uint64_t pol_a = p.a_is_weight ? pol_w : pol_x, pol_b = p.a_is_weight ? pol_x : pol_w;
+    for (int kb = kb0, i = 0; kb < kb1; ++kb, ++i) {
+      const int s = i % STAGES;
+      mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+      mbar_arrive_expect_tx(&full[s], A_BYTES + B_BYTES);
+      tma_load_2d(sa + s * A_BYTES, &tm_a, &full[s], kb * BK, m0, pol_a);
+      tma_load_2d(sb + s * B_BYTES, &tm_b, &full[s], kb * BK, n0, pol_b);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // MMA issuer: 4 x (128 x BN x 16) per 64-wide K block
+    constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+    for (int kb = kb0, i = 0; kb < kb1; ++kb, ++i) {
+      const int s = i % STAGES;
+      mbar_wait(&full[s], (i / STAGES) & 1);
+      tc_fence_after();
+      const uint64_t ad = umma_desc_sw128(sa + s * A_BYTES);
+      const uint64_t bd = umma_desc_sw128(sb + s * B_BYTES);
+#pragma unroll
+      for (int kk = 0; kk < BK / 16; ++kk)
+        umma_bf16(tmem, ad + 2 * kk, bd + 2 * kk, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+      umma_commit(&empty[s]);
+    }
+    umma_commit(accf);
+  }
+  __syncwarp();
+
+  // ---- epilogue: warp w owns TMEM lanes [32w, 32w + 32) = tile rows
+  mbar_wait(accf, 0);
+  tc_fence_after();
+  const int row = warp * 32 + lane;
+  const int m = m0 + row;
+  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+  if (splits == 1) {
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 16) {
+      float v[16];
+      tmem_ld16(trow + c, v);
+      store_chunk<BN>(p, m, n0 + c, v);
+    }
+  } else {
+    const int tile = blockIdx.y * gridDim.x + blockIdx.x;
+    float *mine = p.ws + ((size_t)(tile * splits + split) * BM + row) * BN;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 16) {
+      float v[16];
+      tmem_ld16(trow + c, v);
+#pragma unroll
+      for (int j = 0; j < 16; j += 4) __stcg(reinterpret_cast<float4 *>(mine + c + j), make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int t = atomicAdd(&p.counters[tile], 1);
+      s_last = (t == splits - 1);
+      if (s_last) p.counters[tile] = 0;  // re-arm for the next launch / graph replay
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      const float *base = p.ws + ((size_t)tile * splits * BM + row) * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 16) {
+        float acc[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+        for (int s = 0; s < splits; ++s) {
+          const float *src = base + (size_t)s * BM * BN + c;
+#pragma unroll
+          for (int j = 0; j < 16; j += 4) {
+            float4 f = __ldcg(reinterpret_cast<const float4 *>(src + j));
+            acc[j] += f.x; acc[j + 1] += f.y; acc[j + 2] += f.z; acc[j + 3] += f.w;
+          }
+        }
+        store_chunk<BN>(p, m, n0 + c, acc);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, TMEM_COLS);
+}
+
+// ------------------------------------------------------------------ fp32 SIMT
+// Y[t, n] = sum_k X[t, k] W[n, k]; 64x64 tile, 256 threads x (4x4).
+__global__ void __launch_bounds__(256)
+    gemm_f32_simt_kernel(const float *__restrict__ w, const float *__restrict__ x, float *y,
+                         int n_tok, int n_out, int K, int ldy, int accumulate) {
+  __shared__ float xs[16][64 + 4];
+  __shared__ float ws[16][64 + 4];
+  const int t0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += 16) {
+    for (int i = threadIdx.x; i < 64 * 16; i += 256) {
+      const int r = i / 16, kk = i % 16;
+      const int t = t0 + r, n = n0 + r, k = k0 + kk;
+      xs[kk][r] = (t < n_tok && k < K) ? x[(size_t)t * K + k] : 0.f;
+      ws[kk][r] = (n < n_out && k < K) ? w[(size_t)n * K + k] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        a[i] = xs[kk][ty * 4 + i];
+        b[i] = ws[kk][tx * 4 + i];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int t = t0 + ty * 4 + i;
+    if (t >= n_tok) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + tx * 4 + j;
+      if (n < n_out) {
+        float *dst = y + (size_t)t * ldy + n;
+        *dst = accumulate ? *dst + acc[i][j] : acc[i][j];
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ host side
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+static std::once_flag g_encode_once;
+
+static int get_encode() {
+  std::call_once(g_encode_once, [] {
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  return g_encode ? 0 : HX_ERR_DRIVER;
+}
+
+// 2-D bf16 tensor [rows, cols] row-major with row pitch `pitch` elements;
+// box = box_rows x 64 columns, 128B swizzle.
+static int make_map(CUtensorMap *map, const void *ptr, int rows, int cols, long pitch, int box_rows) {
+  if (get_encode()) return HX_ERR_DRIVER;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)pitch * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims, strides,
+                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : HX_ERR_DRIVER;
+}
+
+template <int BN, int STAGES>
+static size_t smem_bytes() {
+  return 1024 + STAGES * (BM * BK * 2 + BN * BK * 2) + (2 * STAGES + 1) * 8 + 16;
+}
+
+template <int BN, int STAGES>
+static int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, const GemmArgs &p, int splits,
+                     cudaStream_t st) {
+  const size_t smem = smem_bytes<BN, STAGES>();
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaFuncSetAttribute(gemm_bf16_tc_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    attr_done = true;
+  }
+  dim3 grid((p.M + BM - 1) / BM, (p.N + BN - 1) / BN, splits);
+  gemm_bf16_tc_kernel<BN, STAGES><<<grid, 128, smem, st>>>(ma, mb, p);
+  return launch_status();
+}
+
+struct Plan {
+  bool decode;
+  int bn;
+  int splits;
+  int kb_per;
+  int tiles;
+};
+
+static Plan plan_gemm(int n_tok, int n_out, int K) {
+  Plan pl{};
+  const int kb = (K + BK - 1) / BK;
+  pl.decode = n_tok <= 64;
+  if (pl.decode) {
+    pl.bn = n_tok <= 16 ? 16 : (n_tok <= 32 ? 32 : 64);
+    pl.tiles = (n_out + BM - 1) / BM;
+    const int slots = 2 * kNumSMs;
+    double best = -1.0;
+    pl.splits = 1;
+    pl.kb_per = kb;
+    for (int s = 1; s <= 16; ++s) {
+      const int per = (kb + s - 1) / s;
+      if (per < 4 && s > 1) break;
+      const int se = (kb + per - 1) / per;
+      const int ctas = pl.tiles * se;
+      const double eff = (double)ctas / (double)(((ctas + slots - 1) / slots) * slots);
+      if (eff > best + 0.02) {
+        best = eff;
+        pl.splits = se;
+        pl.kb_per = per;
+      }
+    }
+  } else {
+    pl.bn = 256;
+    pl.tiles = ((n_tok + BM - 1) / BM) * ((n_out + 255) / 256);
+    pl.splits = 1;
+    pl.kb_per = kb;
+  }
+  return pl;
+}
+
+}  // namespace hx
+
+using namespace hx;
+
+extern "C" size_t hx_linear_workspace(int dtype, int n_tok, int n_out, int k_dim) {
+  if (dtype != HX_BF16) return 0;
+  Plan pl = plan_gemm(n_tok, n_out, k_dim);
+  if (pl.splits <= 1) return 0;
+  // fp32 partials + one ticket counter per tile (counters first, 256-aligned)
+  size_t counters = ((size_t)pl.tiles * sizeof(int) + 255) & ~size_t(255);
+  return counters + (size_t)pl.tiles * pl.splits * BM * pl.bn * sizeof(float);
+}
+
+extern "C" int hx_linear(const void *w, const void *x, void *y, int dtype, int y_dtype, int n_tok,
+                         int n_out, int k_dim, int ldy, int flags, void *workspace,
+                         size_t workspace_bytes, hx_stream_t stream) {
+  if (n_tok <= 0 || n_out <= 0 || k_dim <= 0) return n_tok == 0 ? 0 : HX_ERR_ARG;
+  if (!w || !x || !y || ldy < n_out) return HX_ERR_ARG;
+  const int accumulate = flags & 1;
+  cudaStream_t st = as_stream(stream);
+  if (dtype == HX_F32) {
+    if (y_dtype != HX_F32) return HX_ERR_UNSUPPORTED;
+    dim3 grid((n_out + 63) / 64, (n_tok + 63) / 64);
+    gemm_f32_simt_kernel<<<grid, 256, 0, st>>>((const float *)w, (const float *)x, (float *)y, n_tok,
+                                                n_out, k_dim, ldy, accumulate);
+    return launch_status();
+  }
+  if (dtype != HX_BF16) return HX_ERR_ARG;
+  if (k_dim % 8) return HX_ERR_UNSUPPORTED;  // TMA row pitch must be 16B aligned
+  if (accumulate && y_dtype != HX_F32) return HX_ERR_UNSUPPORTED;
+  Plan pl = plan_gemm(n_tok, n_out, k_dim);
+  GemmArgs p{};
+  p.c = y;
+  p.K = k_dim;
+  p.c_bf16 = (y_dtype == HX_BF16);
+  p.accumulate = accumulate;
+  p.kb_total = (k_dim + BK - 1) / BK;
+  p.kb_per_split = pl.kb_per;
+  CUtensorMap ma, mb;
+  int rc;
+  if (pl.decode) {
+    p.M = n_out; p.N = n_tok; p.ldm = 1; p.ldn = ldy; p.a_is_weight = 1;
+    if ((rc = make_map(&ma, w, n_out, k_dim, k_dim, BM))) return rc;
+    if ((rc = make_map(&mb, x, n_tok, k_dim, k_dim, pl.bn))) return rc;
+  } else {
+    p.M = n_tok; p.N = n_out; p.ldm = ldy; p.ldn = 1; p.a_is_weight = 0;
+    if ((rc = make_map(&ma, x, n_tok, k_dim, k_dim, BM))) return rc;
+    if ((rc = make_map(&mb, w, n_out, k_dim, k_dim, pl.bn))) return rc;
+  }
+  if (pl.splits > 1) {
+    const size_t need = hx_linear_workspace(dtype, n_tok, n_out, k_dim);
+    if (!workspace || workspace_bytes < need) return HX_ERR_WORKSPACE;
+    size_t counters = ((size_t)pl.tiles * sizeof(int) + 255) & ~size_t(255);
+    p.counters = reinterpret_cast<int *>(workspace);
+    p.ws = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(workspace) + counters);
+  }
+  switch (pl.bn) {
+    case 16: return launch_tc<16, 6>(ma, mb, p, pl.splits, st);
+    case 32: return launch_tc<32, 6>(ma, mb, p, pl.splits, st);
+    case 64: return launch_tc<64, 5>(ma, mb, p, pl.splits, st);
+    default: return launch_tc<256, 4>(ma, mb, p, pl.splits, st);
+  }
+}

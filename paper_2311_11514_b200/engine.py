@@ -1,0 +1,556 @@
+"""The asymmetric TP/PP stage executor (the runtime the reference only models).
+
+Reference anchors: the plan it executes (``costs.py:43-92``, ``cli.py:95-106``),
+the per-layer math (``PAPER.md:114-154``), TP = 2 all-reduces per layer and
+PP = per-stage TP degree + uneven layer counts with a stage-to-stage
+activation hand-off (``PAPER.md:158-160, 195-197``). The cost model's terms
+(``costs.py:106-176``) are what each piece below replaces with real work.
+
+Structure (one process per GPU in production; see ``comm.py`` for the
+single-process emulation used by parity tests):
+
+* ``RankExecutor`` -- one (stage, TP rank): its weight shards, paged KV cache
+  for its layers, static activation buffers, and the kernel sequence of a
+  layer split into the phases between collectives;
+* ``StageDriver`` -- runs the ranks of one stage in lockstep through
+  attention -> all-reduce -> MLP -> all-reduce, the final norm + vocab-parallel
+  lm_head + cross-rank argmax on the last stage, and the stage hand-off;
+* ``Engine`` -- the request API (``generate`` for a ``TaskSpec``-shaped batch,
+  ``service_time`` for the reference's service-time seam); captures each
+  stage's decode step in a CUDA graph.
+
+All arithmetic happens in ``ops`` (the C-ABI kernels); this module only moves
+pointers, issues collectives and sequences launches.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import ops as _ops
+from .comm import make_comm
+from .config import LlamaConfig
+from .plan import GlobalAssignment, InputError, TaskSpec
+from .topology import Role, pipeline_roles, role_of
+from .weights import _CODES, LAYER_TENSORS, init_tensor, shard_layer, tensor_shape
+
+DTYPES = {"bf16": torch.bfloat16, "fp32": torch.float32}
+
+
+# --------------------------------------------------------------------- weights
+def _device_tensor(cfg, seed, name, layer, device):
+    """Synthetic weights generated on the device (fast path for large models):
+    normal(0, 0.02) (+1 for norm gains) from a per-tensor torch generator."""
+    g = torch.Generator(device=device)
+    g.manual_seed((seed * 1_000_003 + (layer + 1) * 1009 + _CODES[name]) & 0x7FFFFFFFFFFFFFFF)
+    t = torch.randn(tensor_shape(cfg, name), generator=g, device=device, dtype=torch.float32)
+    t.mul_(0.02)
+    if name in ("norm", "ln_attn", "ln_mlp"):
+        t.add_(1.0)
+    return t
+
+
+def _shard_device(cfg, lw, r, tp):
+    H = cfg.hidden_dim
+    hd = cfg.head_dim
+    qn, kn, In = cfg.num_heads * hd // tp, cfg.num_kv_heads * hd // tp, cfg.intermediate // tp
+    return {
+        "wqkv": torch.cat([lw["q"][r * qn:(r + 1) * qn], lw["k"][r * kn:(r + 1) * kn],
+                           lw["v"][r * kn:(r + 1) * kn]], 0),
+        "wo": lw["o"][:, r * qn:(r + 1) * qn],
+        "wgu": torch.cat([lw["gate"][r * In:(r + 1) * In], lw["up"][r * In:(r + 1) * In]], 0),
+        "wdown": lw["down"][:, r * In:(r + 1) * In],
+        "ln_attn": lw["ln_attn"], "ln_mlp": lw["ln_mlp"],
+    }
+
+
+def load_rank_weights(cfg: LlamaConfig, role: Role, dtype: torch.dtype, device, seed: int = 0,
+                      source: str = "host") -> dict:
+    """Weight shards for one role. ``source='host'`` draws the bit-exact
+    numpy stream the CPU oracle uses; ``'device'`` generates on the GPU (same
+    distribution, different bits) for throughput runs of large models."""
+    r, tp = role.tp_rank, role.tp
+    out = {"layers": []}
+
+    def put(x, keep_fp32=False):
+        t = torch.as_tensor(x) if isinstance(x, np.ndarray) else x
+        return t.to(device=device, dtype=torch.float32 if keep_fp32 else dtype).contiguous()
+
+    for l in range(*role.layers):
+        if source == "host":
+            lw = {n: init_tensor(cfg, seed, n, l) for n in LAYER_TENSORS}
+            sh = shard_layer(cfg, lw, r, tp)
+        else:
+            lw = {n: _device_tensor(cfg, seed, n, l, device) for n in LAYER_TENSORS}
+            sh = _shard_device(cfg, lw, r, tp)
+        out["layers"].append({k: put(v, keep_fp32=k.startswith("ln_")) for k, v in sh.items()})
+        del lw, sh
+    gen = (lambda n: init_tensor(cfg, seed, n)) if source == "host" else \
+        (lambda n: _device_tensor(cfg, seed, n, -1, device))
+    if role.is_first:
+        out["embed"] = put(gen("embed"))
+    if role.is_last:
+        out["norm"] = put(gen("norm"), keep_fp32=True)
+        vr = cfg.vocab // tp
+        out["lm_head"] = put(gen("lm_head")[r * vr:(r + 1) * vr])
+    return out
+
+
+# --------------------------------------------------------------------- KV cache
+class PagedKVCache:
+    """Paged K/V for one rank's layers: ``k[layer]`` is
+    [num_blocks, kv_heads_rank, page, head_dim]. Blocks are handed out from a
+    free list; sequence b's table is interleaved across the pool so the
+    kernels' block indirection is always exercised (reference memory term:
+    ``costs.py:168-176``)."""
+
+    def __init__(self, n_layers, batch, max_tokens, hkv, hd, page, dtype, device):
+        self.page = page
+        self.max_blocks = math.ceil(max_tokens / page)
+        self.num_blocks = batch * self.max_blocks
+        shape = (n_layers, self.num_blocks, hkv, page, hd)
+        self.k = torch.zeros(shape, dtype=dtype, device=device)
+        self.v = torch.zeros(shape, dtype=dtype, device=device)
+        self.block_table = torch.zeros(batch, self.max_blocks, dtype=torch.int32, device=device)
+        self.seq_lens = torch.zeros(batch, dtype=torch.int32, device=device)
+        self.free = list(range(self.num_blocks))
+        self.owned: list[int] = []
+        self.batch = batch
+
+    def assign(self, batch: int, tokens: int):
+        """Allocate ceil(tokens / page) blocks per sequence; reset lengths."""
+        self.release()
+        need = math.ceil(tokens / self.page)
+        if need > self.max_blocks or batch > self.batch:
+            raise InputError(f"request needs {need} blocks/seq x {batch}; cache holds "
+                             f"{self.max_blocks} x {self.batch}")
+        table = np.zeros((self.batch, self.max_blocks), dtype=np.int32)
+        for i in range(need):
+            for b in range(batch):
+                blk = self.free.pop(0)
+                table[b, i] = blk
+                self.owned.append(blk)
+        self.block_table.copy_(torch.from_numpy(table))
+        self.seq_lens.zero_()
+
+    def release(self):
+        self.free.extend(self.owned)
+        self.free.sort()
+        self.owned = []
+
+    def nbytes(self) -> int:
+        return 2 * self.k.numel() * self.k.element_size()
+
+
+# --------------------------------------------------------------------- executor
+class RankExecutor:
+    """One (stage, TP rank) of the pipeline: weights, KV pages, buffers, kernels."""
+
+    def __init__(self, cfg: LlamaConfig, role: Role, dtype: torch.dtype, batch: int, max_prompt: int,
+                 max_out: int, device, weights: dict, kernels=None, page_size: int = 64):
+        self.cfg, self.role, self.dtype, self.device = cfg, role, dtype, torch.device(device)
+        self.k = kernels or _ops
+        self.w = weights
+        tp = role.tp
+        self.hq, self.hkv = cfg.num_heads // tp, cfg.num_kv_heads // tp
+        self.hd = cfg.head_dim
+        self.inter = cfg.intermediate // tp
+        self.vr = cfg.vocab // tp
+        self.qkv_n = (self.hq + 2 * self.hkv) * self.hd
+        self.batch, self.max_prompt, self.max_out = batch, max_prompt, max_out
+        self.max_ctx = max_prompt + max_out
+        self.n_layers = role.layers[1] - role.layers[0]
+        H = cfg.hidden_dim
+        T = batch * max_prompt
+        dev, act = self.device, dtype
+        z = lambda *s, dt=act: torch.zeros(*s, dtype=dt, device=dev)  # noqa: E731
+        self.x = z(T, H, dt=torch.float32)
+        self.h = z(T, H)
+        self.qkv = z(T, self.qkv_n)
+        self.q = z(T, self.hq * self.hd)
+        self.attn = z(T, self.hq * self.hd)
+        self.proj = z(T, H, dt=torch.float32)
+        self.gu = z(T, 2 * self.inter)
+        self.a = z(T, self.inter)
+        self.kv = PagedKVCache(self.n_layers, batch, self.max_ctx, self.hkv, self.hd, page_size, dtype, dev)
+        self.ids = torch.zeros(batch, dtype=torch.int32, device=dev)
+        self.prompt = torch.zeros(T, dtype=torch.int32, device=dev)
+        if role.is_last:
+            self.hl = z(batch, H)
+            self.logits = z(batch, self.vr, dt=torch.float32)
+            self.keys = torch.zeros(batch, dtype=torch.int64, device=dev)
+            self.history = torch.zeros(batch, max_out, dtype=torch.int32, device=dev)
+            self.step = torch.zeros(1, dtype=torch.int32, device=dev)
+        # decode-shaped split-K / split-KV scratch (prefill uses none)
+        ws = 0
+        if dev.type == "cuda":
+            for n_out, kd in ((self.qkv_n, H), (H, self.hq * self.hd), (2 * self.inter, H),
+                              (H, self.inter), (self.vr, H)):
+                ws = max(ws, self.k.linear_workspace(dtype, batch, n_out, kd))
+            self.attn_ws_bytes = self.k.attn_decode_workspace(batch, self.hq, self.hkv, self.hd, self.max_ctx)
+        else:
+            self.attn_ws_bytes = 0
+        self.lin_ws = torch.zeros(max(ws, 256) // 4 + 64, dtype=torch.int32, device=dev)
+        self.attn_ws = torch.zeros(max(self.attn_ws_bytes, 256) // 4 + 64, dtype=torch.int32, device=dev)
+
+    # ---- phases of layer li (local index) between the two all-reduces
+    def attn_block(self, li: int, n_tok: int, prefill_len: int):
+        k, cfg, lw = self.k, self.cfg, self.w["layers"][li]
+        if li == 0:  # input norm of the stage's first layer (x arrived raw)
+            k.rmsnorm(self.x, lw["ln_attn"], self.h, n_tok, cfg.rms_eps)
+        k.linear(lw["wqkv"], self.h, self.qkv, n_tok, self.lin_ws)
+        kc, vc = self.kv.k[li], self.kv.v[li]
+        k.rope_kv_append(self.qkv, self.q, kc, vc, self.kv.block_table, self.kv.seq_lens, n_tok,
+                         prefill_len, self.hq, self.hkv, self.hd, cfg.rope_theta)
+        if prefill_len:
+            k.attn_prefill(self.q, kc, vc, self.kv.block_table, self.kv.seq_lens, self.attn,
+                           n_tok // prefill_len, prefill_len, self.hq, self.hkv, self.hd)
+        else:
+            k.attn_decode(self.q, kc, vc, self.kv.block_table, self.kv.seq_lens, self.attn, n_tok,
+                          self.hq, self.hkv, self.hd, self.max_ctx, self.attn_ws)
+        k.linear(lw["wo"], self.attn, self.proj, n_tok, self.lin_ws)   # row-parallel partial
+
+    def mlp_block(self, li: int, n_tok: int):
+        k, cfg, lw = self.k, self.cfg, self.w["layers"][li]
+        k.residual_add_rmsnorm(self.x, self.proj, lw["ln_mlp"], self.h, n_tok, cfg.rms_eps)
+        k.linear(lw["wgu"], self.h, self.gu, n_tok, self.lin_ws)
+        k.swiglu(self.gu, self.a, n_tok)
+        k.linear(lw["wdown"], self.a, self.proj, n_tok, self.lin_ws)   # row-parallel partial
+
+    def post_block(self, li: int, n_tok: int):
+        nxt = self.w["layers"][li + 1]["ln_attn"] if li + 1 < self.n_layers else None
+        self.k.residual_add_rmsnorm(self.x, self.proj, nxt, self.h if nxt is not None else None, n_tok,
+                                    self.cfg.rms_eps)
+
+    def head(self, prefill_len: int):
+        """final norm on each sequence's last row + vocab-parallel lm_head + local argmax."""
+        k, H, b = self.k, self.cfg.hidden_dim, self.batch
+        if prefill_len:
+            xs = self.x.view(-1)[(prefill_len - 1) * H:]
+            k.rmsnorm(xs, self.w["norm"], self.hl, b, self.cfg.rms_eps, ldx=prefill_len * H)
+        else:
+            k.rmsnorm(self.x, self.w["norm"], self.hl, b, self.cfg.rms_eps)
+        k.linear(self.w["lm_head"], self.hl, self.logits, b, self.lin_ws)
+        k.argmax_partial(self.logits, self.keys, b, self.vr, self.role.tp_rank * self.vr)
+
+    def finalize(self):
+        self.k.argmax_finalize(self.keys, self.ids, self.history, self.step, self.batch, bump=True)
+
+
+# --------------------------------------------------------------------- driver
+class StageDriver:
+    """Runs the TP ranks of one stage (all of them when emulated in one
+    process, or the single local one under torch.distributed)."""
+
+    def __init__(self, execs: list[RankExecutor], comm, stage: int):
+        self.execs, self.comm, self.stage = execs, comm, stage
+        self.role = execs[0].role
+        self.tp = self.role.tp
+
+    def _ar(self, n_tok):
+        if self.tp > 1:
+            self.comm.all_reduce_sum([e.proj[:n_tok] for e in self.execs], self.role.tp_group)
+
+    def embed(self, n_tok: int, prefill: bool):
+        for e in self.execs:
+            src = e.prompt if prefill else e.ids
+            e.k.embed(src, e.w["embed"], e.x, n_tok)
+
+    def layers(self, n_tok: int, prefill_len: int):
+        for li in range(self.execs[0].n_layers):
+            for e in self.execs:
+                e.attn_block(li, n_tok, prefill_len)
+            self._ar(n_tok)
+            for e in self.execs:
+                e.mlp_block(li, n_tok)
+            self._ar(n_tok)
+            for e in self.execs:
+                e.post_block(li, n_tok)
+        adv = prefill_len if prefill_len else 1
+        for e in self.execs:
+            e.k.advance(e.kv.seq_lens, e.batch, adv)
+
+    def head(self, prefill_len: int):
+        for e in self.execs:
+            e.head(prefill_len)
+        if self.tp > 1:
+            self.comm.all_reduce_max([e.keys for e in self.execs], self.role.tp_group)
+        for e in self.execs:
+            e.finalize()
+
+    def send_hidden(self, n_tok):
+        for e in self.execs:
+            for dst in e.role.send_to:
+                self.comm.send(e.x[:n_tok], e.role.device, dst)
+
+    def recv_hidden(self, n_tok):
+        for e in self.execs:
+            self.comm.recv(e.x[:n_tok], e.role.recv_from, e.role.device)
+
+    def send_ids(self):
+        for e in self.execs:
+            for dst in e.role.ids_send_to:
+                self.comm.send(e.ids, e.role.device, dst)
+
+    def recv_ids(self):
+        for e in self.execs:
+            self.comm.recv(e.ids, e.role.ids_recv_from, e.role.device)
+
+
+# --------------------------------------------------------------------- engine
+@dataclass
+class GenerateResult:
+    ids: np.ndarray                 # [b, s_out] int32
+    prefill_s: float                # device time of the prefill (max over local stages)
+    decode_s: float                 # device time of the s_out - 1 decode steps
+    step_ms: list                   # per decode-step device times (ms)
+    logits: np.ndarray | None = None
+    launches: int = 0               # hx kernels launched (graph replays included)
+
+
+class Engine:
+    """Serve ``TaskSpec``-shaped batches through one pipeline of a plan.
+
+    ``comm='local'`` emulates every rank of the pipeline in this process on
+    ``device`` (parity tests; N=1 benchmarks); ``comm='dist'`` runs the one
+    role whose plan device id equals this process's torch.distributed rank
+    (torchrun, one process per GPU, NCCL)."""
+
+    def __init__(self, plan: GlobalAssignment, cfg: LlamaConfig, *, dtype: str = "bf16",
+                 batch: int, max_prompt: int, max_out: int, pipeline: int = 0, comm: str = "local",
+                 device=None, seed: int = 0, weights: str = "host", page_size: int = 64,
+                 use_graphs: bool = True, kernels=None):
+        if dtype not in DTYPES:
+            raise InputError(f"dtype must be one of {sorted(DTYPES)}")
+        self.plan, self.cfg, self.dtype = plan, cfg, DTYPES[dtype]
+        self.batch, self.max_prompt, self.max_out = batch, max_prompt, max_out
+        self.comm = make_comm(comm)
+        roles = pipeline_roles(plan, pipeline, cfg)
+        self.roles = roles
+        if self.comm.kind == "dist":
+            rank = self.comm.rank
+            pid, me = role_of(plan, rank, cfg)
+            if pid != pipeline:
+                raise InputError(f"rank {rank} has no role in pipeline {pipeline}")
+            local = [me]
+            self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        else:
+            local = roles
+            self.device = torch.device(device) if device is not None else torch.device("cuda", 0)
+        self.comm.setup(roles, local)
+        self.num_stages = roles[0].num_stages
+        self.kernels = kernels or _ops
+        if self.device.type == "cuda":
+            _ops.load()
+        execs = [RankExecutor(cfg, r, self.dtype, batch, max_prompt, max_out, self.device,
+                              load_rank_weights(cfg, r, self.dtype, self.device, seed, weights),
+                              kernels=self.kernels, page_size=page_size) for r in local]
+        self.drivers = []
+        for j in sorted({r.stage for r in local}):
+            self.drivers.append(StageDriver([e for e in execs if e.role.stage == j], self.comm, j))
+        self.execs = execs
+        self.use_graphs = use_graphs and self.device.type == "cuda"
+        self._graphs = None
+        self._graph_key = None
+        self._graph_launches = []
+        self._replayed = 0
+
+    # ---------------------------------------------------------------- steps
+    def _prefill(self, b, s):
+        n = b * s
+        for d in self.drivers:
+            if d.stage == 0:
+                d.embed(n, prefill=True)
+            else:
+                d.recv_hidden(n)
+            d.layers(n, s)
+            if d.stage == self.num_stages - 1:
+                d.head(s)
+            else:
+                d.send_hidden(n)
+
+    def _decode_compute(self, d: StageDriver, b):
+        if d.stage == 0:
+            d.embed(b, prefill=False)
+        d.layers(b, 0)
+        if d.stage == self.num_stages - 1:
+            d.head(0)
+
+    def _return_ids(self):
+        if self.num_stages == 1:
+            return
+        for d in self.drivers:
+            if d.stage == self.num_stages - 1:
+                d.send_ids()
+        for d in self.drivers:
+            if d.stage == 0:
+                d.recv_ids()
+
+    def _decode_step(self, b, graphs=None):
+        self._return_ids()
+        for i, d in enumerate(self.drivers):
+            if d.stage > 0:
+                d.recv_hidden(b)
+            if graphs is not None:
+                graphs[i].replay()
+                self._replayed += self._graph_launches[i]
+            else:
+                self._decode_compute(d, b)
+            if d.stage < self.num_stages - 1:
+                d.send_hidden(b)
+
+    def _capture(self, b):
+        """One CUDA graph per local stage for the decode compute (collectives
+        inside; stage hand-offs stay outside on the same stream)."""
+        key = b
+        if self._graphs is not None and self._graph_key == key:
+            return self._graphs
+        graphs, counts = [], []
+        for d in self.drivers:
+            g = torch.cuda.CUDAGraph()
+            n0 = self._launch_count()
+            with torch.cuda.graph(g):
+                self._decode_compute(d, b)
+            counts.append(self._launch_count() - n0)
+            graphs.append(g)
+        self._graphs, self._graph_key, self._graph_launches = graphs, key, counts
+        return graphs
+
+    def _launch_count(self) -> int:
+        fn = getattr(self.kernels, "launch_count", None)
+        return fn() if fn else 0
+
+    def _reset(self, b, s, s_out):
+        for e in self.execs:
+            e.kv.assign(b, s + s_out)
+            if e.role.is_last:
+                e.step.zero_()
+
+    # ---------------------------------------------------------------- API
+    def generate(self, prompt, output_len: int | None = None, return_logits: bool = False,
+                 forced=None) -> GenerateResult:
+        """Greedy generation (HF ``max_new_tokens`` semantics): the prefill
+        emits token 1, then ``output_len - 1`` decode steps. ``prompt`` is a
+        host int array [b, s_in]; returns host ids [b, output_len] on every
+        rank (broadcast from the last stage under torch.distributed).
+        ``forced`` [b, output_len] teacher-forces the token fed back to stage 0
+        (the bf16-mode tolerance check); the returned ids stay the argmax."""
+        if forced is not None:
+            return_logits = True
+            forced_dev = torch.as_tensor(np.asarray(forced, dtype=np.int32), device=self.device)
+        prompt = np.asarray(prompt, dtype=np.int32)
+        b, s = prompt.shape
+        s_out = output_len or self.max_out
+        if b > self.batch or s > self.max_prompt or s_out > self.max_out:
+            raise InputError(f"request {(b, s, s_out)} exceeds engine shape "
+                             f"{(self.batch, self.max_prompt, self.max_out)}")
+        if b != self.batch:
+            raise InputError("static batching: batch must equal the engine batch")
+        cuda = self.device.type == "cuda"
+        if cuda and self.use_graphs and not return_logits:
+            # warm the eager path once (kernel attributes, NCCL comms) before capture
+            if self._graphs is None:
+                self._reset(b, s, s_out)
+                for e in self.execs:
+                    if e.role.is_first:
+                        e.prompt[:b * s].copy_(torch.from_numpy(prompt.reshape(-1)))
+                self._prefill(b, s)
+                self._return_ids()
+                for d in self.drivers:
+                    if d.stage > 0:
+                        d.recv_hidden(b)
+                    self._decode_compute(d, b)
+                    if d.stage < self.num_stages - 1:
+                        d.send_hidden(b)
+                torch.cuda.synchronize(self.device)
+                self._capture(b)
+        graphs = self._graphs if (cuda and self.use_graphs and not return_logits) else None
+        self._replayed = 0
+        n_launch0 = self._launch_count()
+        self._reset(b, s, s_out)
+        pin = torch.from_numpy(prompt.reshape(-1))
+        if cuda:
+            pin = pin.pin_memory()
+        for e in self.execs:
+            if e.role.is_first:
+                e.prompt[:b * s].copy_(pin, non_blocking=True)
+        logits = [] if return_logits else None
+        ev = (lambda: torch.cuda.Event(enable_timing=True)) if cuda else None
+        t0 = ev() if cuda else None
+        if cuda:
+            t0.record()
+        else:
+            w0 = time.perf_counter()
+        self._prefill(b, s)
+        if return_logits:
+            logits.append(self._gather_logits())
+        if forced is not None:
+            self._force(forced_dev, 0)
+        step_ev = []
+        if cuda:
+            t1 = ev()
+            t1.record()
+        else:
+            w1 = time.perf_counter()
+        for t in range(1, s_out):
+            if cuda:
+                e0 = ev()
+                e0.record()
+            self._decode_step(b, graphs)
+            if cuda:
+                e1 = ev()
+                e1.record()
+                step_ev.append((e0, e1))
+            if return_logits:
+                logits.append(self._gather_logits())
+            if forced is not None:
+                self._force(forced_dev, t)
+        if cuda:
+            t2 = ev()
+            t2.record()
+        ids = self._collect_ids(b, s_out)
+        if cuda:
+            torch.cuda.synchronize(self.device)
+            pre = t0.elapsed_time(t1) / 1e3
+            dec = t1.elapsed_time(t2) / 1e3
+            steps = [a.elapsed_time(c) for a, c in step_ev]
+        else:
+            w2 = time.perf_counter()
+            pre, dec, steps = w1 - w0, w2 - w1, []
+        lg = np.stack(logits, 0) if return_logits else None
+        launches = self._launch_count() - n_launch0 + self._replayed
+        return GenerateResult(ids, pre, dec, steps, lg, launches)
+
+    def _force(self, forced_dev, t):
+        for e in self._last_execs():
+            e.ids.copy_(forced_dev[:, t])
+
+    def _last_execs(self):
+        return [e for e in self.execs if e.role.is_last]
+
+    def _gather_logits(self):
+        last = sorted(self._last_execs(), key=lambda e: e.role.tp_rank)
+        if not last:
+            return None
+        if len(last) == last[0].role.tp:
+            return torch.cat([e.logits for e in last], dim=-1).float().cpu().numpy()
+        return self.comm.gather_logits(last[0])
+
+    def _collect_ids(self, b, s_out):
+        last = self._last_execs()
+        hist = last[0].history[:b, :s_out] if last else None
+        return self.comm.broadcast_ids(hist, b, s_out, self.roles[-1].tp_group[0], self.device)
+
+    def service_time(self, task: TaskSpec, prompt=None) -> float:
+        """Measured seconds for one request of this shape (the value the
+        reference's ``service_times`` table holds, simulate.py:135-142)."""
+        if prompt is None:
+            rng = np.random.default_rng(1)
+            prompt = rng.integers(0, self.cfg.vocab, size=(task.batch_size, task.input_len), dtype=np.int32)
+        r = self.generate(prompt, task.output_len)
+        return r.prefill_s + r.decode_s

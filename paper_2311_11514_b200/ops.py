@@ -1,0 +1,180 @@
+"""ctypes bindings to ``libhexgen.so`` (the C-ABI in ``include/hx_api.h``).
+
+Torch tensors are used only as device memory: each wrapper passes raw data
+pointers, sizes and the current CUDA stream across the C boundary. There is
+no fallback -- if the library is missing or a call fails, these functions
+raise (``HxError``); the data path has no CPU or eager-PyTorch substitute.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from pathlib import Path
+
+import torch
+
+LIB_PATH = Path(__file__).resolve().parent / "libhexgen.so"
+HX_F32, HX_BF16 = 0, 1
+
+_lib = None
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_F = ctypes.c_float
+_SZ = ctypes.c_size_t
+
+_SIGS = {
+    "hx_version": ([], _I),
+    "hx_error_string": ([_I], ctypes.c_char_p),
+    "hx_launch_count": ([], ctypes.c_uint64),
+    "hx_embed": ([_P, _P, _I, _P, _I, _I, _I, _P], _I),
+    "hx_rmsnorm": ([_P, _I, _P, _P, _I, _I, _I, _F, _P], _I),
+    "hx_residual_add_rmsnorm": ([_P, _P, _P, _P, _I, _I, _I, _F, _P], _I),
+    "hx_linear": ([_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _SZ, _P], _I),
+    "hx_linear_workspace": ([_I, _I, _I, _I], _SZ),
+    "hx_swiglu": ([_P, _P, _I, _I, _I, _P], _I),
+    "hx_rope_kv_append": ([_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _F, _P], _I),
+    "hx_attn_decode_paged": ([_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _SZ, _P], _I),
+    "hx_attn_decode_workspace": ([_I, _I, _I, _I, _I], _SZ),
+    "hx_attn_prefill": ([_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P], _I),
+    "hx_advance": ([_P, _I, _I, _P], _I),
+    "hx_argmax_partial": ([_P, _P, _I, _I, _I, _I, _P], _I),
+    "hx_argmax_finalize": ([_P, _P, _P, _P, _I, _I, _I, _P], _I),
+    "hx_kv_bytes": ([_I, _I, _I, _I, _I, _I], _SZ),
+}
+
+EXPORTED = tuple(_SIGS)
+
+
+class HxError(RuntimeError):
+    pass
+
+
+def load(path: Path | str | None = None):
+    """Load the C-ABI library; raises if it has not been built."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise HxError(f"{p} not built -- run `python -m paper_2311_11514_b200.build` "
+                      "(there is no CPU fallback for the data path)")
+    lib = ctypes.CDLL(str(p))
+    for name, (args, res) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        msg = load().hx_error_string(rc).decode()
+        raise HxError(f"{what} failed: {msg} (code {rc})")
+
+
+def dtype_code(dt: torch.dtype) -> int:
+    if dt == torch.float32:
+        return HX_F32
+    if dt == torch.bfloat16:
+        return HX_BF16
+    raise HxError(f"unsupported dtype {dt}")
+
+
+def _p(t):
+    return None if t is None else t.data_ptr()
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def launch_count() -> int:
+    return int(load().hx_launch_count())
+
+
+def embed(ids, table, x, n_tok):
+    _check(load().hx_embed(_p(ids), _p(table), dtype_code(table.dtype), _p(x), n_tok,
+                           table.shape[1], table.shape[0], _stream()), "hx_embed")
+
+
+def rmsnorm(x, gain, out, n_tok, eps, ldx=None):
+    H = gain.shape[0]
+    _check(load().hx_rmsnorm(_p(x), ldx or H, _p(gain), _p(out), dtype_code(out.dtype), n_tok, H,
+                             eps, _stream()), "hx_rmsnorm")
+
+
+def residual_add_rmsnorm(x, delta, gain, out, n_tok, eps):
+    H = x.shape[-1]
+    _check(load().hx_residual_add_rmsnorm(_p(x), _p(delta), _p(gain), _p(out),
+                                          dtype_code(out.dtype) if out is not None else HX_F32,
+                                          n_tok, H, eps, _stream()), "hx_residual_add_rmsnorm")
+
+
+def linear_workspace(dtype, n_tok, n_out, k_dim) -> int:
+    return int(load().hx_linear_workspace(dtype_code(dtype), n_tok, n_out, k_dim))
+
+
+def linear(w, x, y, n_tok, workspace=None, accumulate=False):
+    """y[:n_tok, :n_out] (+)= x[:n_tok] @ w.T ; w [n_out, K] row-major."""
+    n_out, k = w.shape
+    ws = workspace
+    _check(load().hx_linear(_p(w), _p(x), _p(y), dtype_code(w.dtype), dtype_code(y.dtype), n_tok,
+                            n_out, k, y.shape[-1], 1 if accumulate else 0, _p(ws),
+                            0 if ws is None else ws.numel() * ws.element_size(), _stream()),
+           "hx_linear")
+
+
+def swiglu(gu, out, n_tok):
+    _check(load().hx_swiglu(_p(gu), _p(out), dtype_code(gu.dtype), n_tok, out.shape[-1], _stream()),
+           "hx_swiglu")
+
+
+def rope_kv_append(qkv, q_out, k_cache, v_cache, block_table, seq_lens, n_tok, prefill_len,
+                   hq, hkv, hd, theta):
+    page = k_cache.shape[2]
+    _check(load().hx_rope_kv_append(_p(qkv), _p(q_out), _p(k_cache), _p(v_cache), _p(block_table),
+                                    _p(seq_lens), dtype_code(qkv.dtype), n_tok, prefill_len, hq, hkv,
+                                    hd, page, block_table.shape[1], theta, _stream()),
+           "hx_rope_kv_append")
+
+
+def attn_decode_workspace(batch, hq, hkv, hd, max_ctx) -> int:
+    return int(load().hx_attn_decode_workspace(batch, hq, hkv, hd, max_ctx))
+
+
+def attn_decode(q, k_cache, v_cache, block_table, seq_lens, o, batch, hq, hkv, hd, max_ctx,
+                workspace=None):
+    ws = workspace
+    _check(load().hx_attn_decode_paged(_p(q), _p(k_cache), _p(v_cache), _p(block_table), _p(seq_lens),
+                                       _p(o), dtype_code(q.dtype), batch, hq, hkv, hd, k_cache.shape[2],
+                                       block_table.shape[1], max_ctx, _p(ws),
+                                       0 if ws is None else ws.numel() * ws.element_size(), _stream()),
+           "hx_attn_decode_paged")
+
+
+def attn_prefill(q, k_cache, v_cache, block_table, seq_lens, o, batch, s, hq, hkv, hd):
+    _check(load().hx_attn_prefill(_p(q), _p(k_cache), _p(v_cache), _p(block_table), _p(seq_lens), _p(o),
+                                  dtype_code(q.dtype), batch, s, hq, hkv, hd, k_cache.shape[2],
+                                  block_table.shape[1], _stream()), "hx_attn_prefill")
+
+
+def advance(seq_lens, batch, n):
+    _check(load().hx_advance(_p(seq_lens), batch, n, _stream()), "hx_advance")
+
+
+def argmax_partial(logits, keys, n_tok, n_cols, vocab_offset):
+    _check(load().hx_argmax_partial(_p(logits), _p(keys), n_tok, n_cols, logits.shape[-1], vocab_offset,
+                                    _stream()), "hx_argmax_partial")
+
+
+def argmax_finalize(keys, ids, history, step, n_tok, bump=True):
+    s_out = history.shape[1] if history is not None else 0
+    _check(load().hx_argmax_finalize(_p(keys), _p(ids), _p(history), _p(step), s_out, n_tok,
+                                     1 if bump else 0, _stream()), "hx_argmax_finalize")
+
+
+def kv_bytes(dtype, layers, num_blocks, hkv_rank, page, hd) -> int:
+    return int(load().hx_kv_bytes(dtype_code(dtype), layers, num_blocks, hkv_rank, page, hd))

@@ -1,0 +1,45 @@
+"""Engine host logic on CPU (test kernels in tests/cpu_kernels.py, LocalComm):
+asymmetric plans reproduce the HF-pinned greedy ids of the tiny config."""
+
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import cpu_kernels
+from paper_2311_11514_b200.config import TINY
+from paper_2311_11514_b200.engine import Engine, PagedKVCache
+from paper_2311_11514_b200.plan import InputError, TaskSpec, simple_plan
+
+G = np.load(Path(__file__).parent / "golden" / "tiny_hf.npz")
+
+
+@pytest.mark.parametrize("tps,layers", [([2, 1], [3, 1]), ([1], [4]), ([1, 2, 4], [1, 1, 2])])
+def test_asymmetric_plans_match_golden(tps, layers):
+    eng = Engine(simple_plan(tps, layers), TINY, dtype="fp32", batch=2, max_prompt=64, max_out=16,
+                 device="cpu", kernels=cpu_kernels, page_size=16)
+    r = eng.generate(G["prompt"], 16, return_logits=True)
+    assert np.array_equal(r.ids, G["ids"])
+    assert np.abs(r.logits[..., G["cols"]] - G["col_val"]).max() / G["max_abs"] < 1e-3
+
+
+def test_request_shape_checks():
+    eng = Engine(simple_plan([1], [4]), TINY, dtype="fp32", batch=2, max_prompt=8, max_out=4,
+                 device="cpu", kernels=cpu_kernels, page_size=16)
+    with pytest.raises(InputError):
+        eng.generate(np.zeros((2, 9), np.int32), 4)
+    with pytest.raises(InputError):
+        eng.generate(np.zeros((1, 8), np.int32), 4)
+    t = eng.service_time(TaskSpec(2, 8, 3))
+    assert t > 0
+
+
+def test_kv_pages_are_interleaved_and_recycled():
+    kv = PagedKVCache(1, 3, 40, 2, 8, 16, __import__("torch").float32, "cpu")
+    kv.assign(3, 40)
+    bt = kv.block_table.numpy()
+    assert bt[:, 0].tolist() == [0, 1, 2] and bt[:, 1].tolist() == [3, 4, 5]
+    with pytest.raises(InputError):
+        kv.assign(3, 100)
+    kv.assign(2, 16)
+    assert len(kv.owned) == 2 and len(kv.free) == kv.num_blocks - 2
