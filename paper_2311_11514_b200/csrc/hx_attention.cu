@@ -365,7 +365,7 @@ extern "C" int hx_rope_kv_append(const void *qkv, void *q_out, void *k_cache, vo
 extern "C" size_t hx_attn_decode_workspace(int batch, int hq, int hkv, int hd, int max_ctx) {
   const int s = decode_splits(batch, hkv, max_ctx);
   if (s <= 1) return 0;
-  const size_t counters = ((size_t)batch * hkv * sizeof(int) + 255) & ~size_t(255);
+  const size_t counters = kTicketBytes;
   return counters + (size_t)batch * hkv * s * (hq / hkv) * (hd + 2) * sizeof(float);
 }
 
@@ -382,7 +382,8 @@ extern "C" int hx_attn_decode_paged(const void *q, const void *k_cache, const vo
   if (splits > 1) {
     if (!workspace || workspace_bytes < hx_attn_decode_workspace(batch, hq, hkv, hd, max_ctx))
       return HX_ERR_WORKSPACE;
-    const size_t counters = ((size_t)batch * hkv * sizeof(int) + 255) & ~size_t(255);
+    if (batch * hkv > kMaxTickets) return HX_ERR_UNSUPPORTED;
+    const size_t counters = kTicketBytes;
     cnt = reinterpret_cast<int *>(workspace);
     ws = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(workspace) + counters);
   }

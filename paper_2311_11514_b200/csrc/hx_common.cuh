@@ -13,6 +13,12 @@ namespace hx {
 
 extern unsigned long long g_launches;
 
+// Every split-K / split-KV workspace starts with a fixed-size array of ticket
+// counters (zeroed once by the caller, re-armed by the kernels), so kernels of
+// different shapes sharing one workspace never overlay partials on tickets.
+constexpr size_t kTicketBytes = 16384;
+constexpr int kMaxTickets = (int)(kTicketBytes / sizeof(int));
+
 inline int launch_status() {
   cudaError_t e = cudaGetLastError();
   ++g_launches;
@@ -82,16 +88,20 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
                "r"(bytes)
                : "memory");
 }
+// Bounded wait: a pipeline bug traps (kernel error) instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\t"
-      "HX_WAIT:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@P1 bra HX_DONE;\n\t"
-      "bra HX_WAIT;\n\t"
-      "HX_DONE:\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
+  uint32_t done = 0;
+  for (uint32_t spins = 0;; ++spins) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (spins > (1u << 28)) __trap();
+  }
 }
 
 // ---------------------------------------------------------------- PTX: TMA

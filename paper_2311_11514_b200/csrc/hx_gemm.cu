@@ -342,7 +342,7 @@ extern "C" size_t hx_linear_workspace(int dtype, int n_tok, int n_out, int k_dim
   Plan pl = plan_gemm(n_tok, n_out, k_dim);
   if (pl.splits <= 1) return 0;
   // fp32 partials + one ticket counter per tile (counters first, 256-aligned)
-  size_t counters = ((size_t)pl.tiles * sizeof(int) + 255) & ~size_t(255);
+  const size_t counters = kTicketBytes;
   return counters + (size_t)pl.tiles * pl.splits * BM * pl.bn * sizeof(float);
 }
 
@@ -385,7 +385,8 @@ extern "C" int hx_linear(const void *w, const void *x, void *y, int dtype, int y
   if (pl.splits > 1) {
     const size_t need = hx_linear_workspace(dtype, n_tok, n_out, k_dim);
     if (!workspace || workspace_bytes < need) return HX_ERR_WORKSPACE;
-    size_t counters = ((size_t)pl.tiles * sizeof(int) + 255) & ~size_t(255);
+    if (pl.tiles > kMaxTickets) return HX_ERR_UNSUPPORTED;
+    const size_t counters = kTicketBytes;
     p.counters = reinterpret_cast<int *>(workspace);
     p.ws = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(workspace) + counters);
   }

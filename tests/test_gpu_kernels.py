@@ -52,6 +52,23 @@ def test_linear_bf16(n_tok, n_out, k, ydt):
     assert torch.equal(y, y2)
 
 
+def test_linear_shared_workspace_across_shapes():
+    """The engine shares one split-K workspace across GEMMs of different tile
+    counts; a small-tile GEMM must not clobber the big one's tickets."""
+    shapes = [(8, 4096, 4096), (8, 12288, 4096), (8, 4096, 11008), (8, 22016, 4096), (8, 32000, 4096)]
+    ws = torch.zeros(max(ops.linear_workspace(torch.bfloat16, *s) for s in shapes) // 4 + 64,
+                     dtype=torch.int32, device=DEV)
+    for _ in range(2):
+        for n_tok, n_out, k in shapes:
+            w = (torch.randn(n_out, k, device=DEV) * 0.02).bfloat16()
+            x = torch.randn(64, k, device=DEV).bfloat16()   # buffer taller than n_tok
+            y = torch.zeros(64, n_out, device=DEV)
+            ops.linear(w, x, y, n_tok, ws)
+            torch.cuda.synchronize()
+            assert rel_err(y[:n_tok], x[:n_tok].float() @ w.float().T) < 1e-3
+            assert not y[n_tok:].any()
+
+
 def test_linear_bf16_accumulate_and_pitch():
     w = (torch.randn(512, 256, device=DEV) * 0.05).bfloat16()
     x = torch.randn(8, 256, device=DEV).bfloat16()
