@@ -75,12 +75,24 @@ int hx_residual_add_rmsnorm(float *x, const float *delta, const float *gain,
 /* Y[t, n] (+)= sum_k X[t, k] W[n, k], t < n_tok, n < n_out, k < k_dim.
  * bf16 weights+activations: tcgen05/TMEM tensor-core kernel fed by TMA
  * (split-K for decode-sized n_tok, fp32 accumulate); fp32: CUDA-core kernel.
- * y_dtype HX_F32 or HX_BF16; ldy = row pitch of Y in elements; flags bit0:
- * accumulate into Y (fp32 Y only). workspace >= hx_linear_workspace(...). */
+ * y_dtype HX_F32 or HX_BF16; ldy = row pitch of Y in elements; flags:
+ * HX_LINEAR_ACCUMULATE (Y += .., fp32 Y only), HX_LINEAR_PACKED (w is in the
+ * hx_pack_weight tile layout). workspace >= hx_linear_workspace(...), its
+ * first 16 KB (ticket counters) zeroed once before first use. */
+enum hx_linear_flags { HX_LINEAR_ACCUMULATE = 1, HX_LINEAR_PACKED = 2 };
 int hx_linear(const void *w, const void *x, void *y, int dtype, int y_dtype,
               int n_tok, int n_out, int k_dim, int ldy, int flags,
               void *workspace, size_t workspace_bytes, hx_stream_t stream);
 size_t hx_linear_workspace(int dtype, int n_tok, int n_out, int k_dim);
+
+/* Repack a bf16 weight [n_out, k_dim] into [ceil(n/128)][ceil(k/64)][128][64]
+ * tiles (zero padded) so each 16 KB tile the decode GEMM streams is one
+ * contiguous HBM range; packed holds hx_packed_weight_elems(n_out, k_dim). */
+int hx_pack_weight(const void *w, void *packed, int n_out, int k_dim, hx_stream_t stream);
+size_t hx_packed_weight_elems(int n_out, int k_dim);
+
+/* Programmatic dependent launch on/off for subsequent launches (default on). */
+void hx_set_pdl(int enabled);
 
 /* out[t, j] = silu(gu[t, j]) * gu[t, inter + j], j < inter */
 int hx_swiglu(const void *gu, void *out, int dtype, int n_tok, int inter,

@@ -91,36 +91,43 @@ def attention(q, k, v, causal_offset):
 
 
 class Oracle:
-    """Unsharded fp32 Llama forward with a KV cache."""
+    """Unsharded fp32 Llama forward with a KV cache.
 
-    def __init__(self, cfg, weights):
+    ``act_bf16=True`` additionally rounds to bf16 exactly where the bf16-mode
+    engine stores bf16 (norm outputs, qkv, roped q/k and v in the cache,
+    attention output, gate/up and SwiGLU outputs); the residual stream, the
+    row-parallel outputs and logits stay fp32 as in the engine."""
+
+    def __init__(self, cfg, weights, act_bf16=False):
         self.cfg = cfg
         self.w = weights
+        self.r = bf16_round if act_bf16 else (lambda a: a)
 
     def layer(self, l, x, pos0, cache):
         cfg, lw = self.cfg, self.w["layers"][l]
         b, s, H = x.shape
         hd, hq, hkv = cfg.head_dim, cfg.num_heads, cfg.num_kv_heads
-        h = rmsnorm(x, lw["ln_attn"], cfg.rms_eps)
-        q = lin(h, lw["q"]).reshape(b, s, hq, hd).transpose(0, 2, 1, 3)
-        k = lin(h, lw["k"]).reshape(b, s, hkv, hd).transpose(0, 2, 1, 3)
-        v = lin(h, lw["v"]).reshape(b, s, hkv, hd).transpose(0, 2, 1, 3)
+        r = self.r
+        h = r(rmsnorm(x, lw["ln_attn"], cfg.rms_eps))
+        q = r(lin(h, lw["q"])).reshape(b, s, hq, hd).transpose(0, 2, 1, 3)
+        k = r(lin(h, lw["k"])).reshape(b, s, hkv, hd).transpose(0, 2, 1, 3)
+        v = r(lin(h, lw["v"])).reshape(b, s, hkv, hd).transpose(0, 2, 1, 3)
         cos, sin = rope_tables(hd, cfg.rope_theta, np.arange(pos0, pos0 + s))
-        q, k = apply_rope(q, cos, sin), apply_rope(k, cos, sin)
+        q, k = r(apply_rope(q, cos, sin)), r(apply_rope(k, cos, sin))
         if l in cache.k:
             cache.k[l] = np.concatenate([cache.k[l], k], axis=2)
             cache.v[l] = np.concatenate([cache.v[l], v], axis=2)
         else:
             cache.k[l], cache.v[l] = k, v
-        o = attention(q, cache.k[l], cache.v[l], pos0)
+        o = r(attention(q, cache.k[l], cache.v[l], pos0))
         o = o.transpose(0, 2, 1, 3).reshape(b, s, hq * hd)
         x = (x + lin(o, lw["o"])).astype(F32)
-        h = rmsnorm(x, lw["ln_mlp"], cfg.rms_eps)
-        a = silu(lin(h, lw["gate"])) * lin(h, lw["up"])
+        h = r(rmsnorm(x, lw["ln_mlp"], cfg.rms_eps))
+        a = r(silu(r(lin(h, lw["gate"]))) * r(lin(h, lw["up"])))  # silu in fp32, one rounding
         return (x + lin(a, lw["down"])).astype(F32)
 
     def logits(self, x_last):
-        h = rmsnorm(x_last, self.w["norm"], self.cfg.rms_eps)
+        h = self.r(rmsnorm(x_last, self.w["norm"], self.cfg.rms_eps))
         return lin(h, self.w["lm_head"]).astype(F32)
 
     def forward(self, ids, pos0, cache):

@@ -17,43 +17,38 @@ __device__ __forceinline__ size_t page_index(const int32_t *bt, int b, int pos, 
 }
 
 // ------------------------------------------------------------- RoPE + append
+// grid (token, head of the packed q|k|v row); hd/2 threads, one rotate-half
+// pair each (v heads: plain copy into the page).
 template <typename T>
 __global__ void rope_append_kernel(const T *qkv, T *q_out, T *kc, T *vc, const int32_t *bt,
                                    const int32_t *seq_lens, int prefill_len, int hq, int hkv, int hd,
                                    int page, int max_blocks, float theta) {
-  const int t = blockIdx.x;
+  pdl_trigger();
+  pdl_wait();
+  const int t = blockIdx.x, h = blockIdx.y, i = threadIdx.x;
   const int b = prefill_len ? t / prefill_len : t;
   const int pos = seq_lens[b] + (prefill_len ? t % prefill_len : 0);
   const int half = hd / 2;
-  const int row = (hq + 2 * hkv) * hd;
-  const T *src = qkv + (size_t)t * row;
-  const int n_rope = (hq + hkv) * half;
-  for (int w = threadIdx.x; w < n_rope + hkv * hd; w += blockDim.x) {
-    if (w < n_rope) {
-      const int h = w / half, i = w % half;
-      const float inv_freq = 1.0f / powf(theta, (float)(2 * i) / (float)hd);
-      const float ang = (float)pos * inv_freq;
-      float s, c;
-      sincosf(ang, &s, &c);
-      const float x1 = to_f32(src[h * hd + i]);
-      const float x2 = to_f32(src[h * hd + i + half]);
-      const float y1 = x1 * c - x2 * s;  // x * cos + rotate_half(x) * sin
-      const float y2 = x2 * c + x1 * s;
-      if (h < hq) {
-        T *dst = q_out + ((size_t)t * hq + h) * hd;
-        dst[i] = from_f32<T>(y1);
-        dst[i + half] = from_f32<T>(y2);
-      } else {
-        T *dst = kc + page_index(bt, b, pos, max_blocks, page, hkv, h - hq, hd);
-        dst[i] = from_f32<T>(y1);
-        dst[i + half] = from_f32<T>(y2);
-      }
-    } else {
-      const int v = w - n_rope;
-      const int h = v / hd, d = v % hd;
-      vc[page_index(bt, b, pos, max_blocks, page, hkv, h, hd) + d] = src[(hq + hkv) * hd + v];
-    }
+  const T *src = qkv + (size_t)t * (hq + 2 * hkv) * hd + (size_t)h * hd;
+  if (i >= half) return;
+  if (h >= hq + hkv) {
+    T *dst = vc + page_index(bt, b, pos, max_blocks, page, hkv, h - hq - hkv, hd);
+    dst[i] = src[i];
+    dst[i + half] = src[i + half];
+    return;
   }
+  const float inv_freq = 1.0f / powf(theta, (float)(2 * i) / (float)hd);
+  const float ang = (float)pos * inv_freq;
+  float sn, cs;
+  sincosf(ang, &sn, &cs);
+  const float x1 = to_f32(src[i]);
+  const float x2 = to_f32(src[i + half]);
+  const float y1 = x1 * cs - x2 * sn;  // x * cos + rotate_half(x) * sin
+  const float y2 = x2 * cs + x1 * sn;
+  T *dst = h < hq ? q_out + ((size_t)t * hq + h) * hd
+                  : kc + page_index(bt, b, pos, max_blocks, page, hkv, h - hq, hd);
+  dst[i] = from_f32<T>(y1);
+  dst[i + half] = from_f32<T>(y2);
 }
 
 // ------------------------------------------------------------- decode
@@ -67,11 +62,13 @@ template <typename T, int HD, int G>
 __global__ void __launch_bounds__(DEC_THREADS)
     attn_decode_kernel(const T *q, const T *kc, const T *vc, const int32_t *bt, const int32_t *seq_lens,
                        T *o, int hkv, int page, int max_blocks, float scale, float *ws, int *counters) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int V = Vec16<T>::N;
   constexpr int LG = HD / V;
   constexpr int GPW = 32 / LG;
   constexpr int NG = (DEC_THREADS / 32) * GPW;
-  constexpr int U = 4;
+  constexpr int U = G <= 2 ? 8 : 4;  // 2*U independent 16-byte loads in flight per lane
   const int b = blockIdx.x / hkv, kvh = blockIdx.x % hkv;
   const int split = blockIdx.y, splits = gridDim.y;
   const int hq = hkv * G;
@@ -99,7 +96,7 @@ __global__ void __launch_bounds__(DEC_THREADS)
   }
   const int32_t *btb = bt + (size_t)b * max_blocks;
   for (int base = t0; base < t1; base += NG * U) {  // warp-uniform trip count (shuffles below)
-    float kv[U][V], vv[U][V];
+    uint4 kraw[U], vraw[U];  // raw 16-byte vectors: all loads issued before any use
     bool ok[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -107,18 +104,24 @@ __global__ void __launch_bounds__(DEC_THREADS)
       ok[u] = p < t1;
       if (ok[u]) {
         const size_t off = (((size_t)btb[p / page] * hkv + kvh) * page + p % page) * HD + d0;
-        Vec16<T>::load(kc + off, kv[u]);
-        Vec16<T>::load(vc + off, vv[u]);
+        kraw[u] = __ldg(reinterpret_cast<const uint4 *>(kc + off));
+        vraw[u] = __ldg(reinterpret_cast<const uint4 *>(vc + off));
+      } else {
+        kraw[u] = make_uint4(0, 0, 0, 0);
+        vraw[u] = make_uint4(0, 0, 0, 0);
       }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
+      float kv[V], vv[V];
+      Vec16<T>::load(reinterpret_cast<const T *>(&kraw[u]), kv);
+      Vec16<T>::load(reinterpret_cast<const T *>(&vraw[u]), vv);
       float s[G];
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         float a = 0.f;
 #pragma unroll
-        for (int j = 0; j < V; ++j) a = fmaf(qv[g][j], kv[u][j], a);
+        for (int j = 0; j < V; ++j) a = fmaf(qv[g][j], kv[j], a);
 #pragma unroll
         for (int off = LG / 2; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
         s[g] = a;
@@ -131,7 +134,7 @@ __global__ void __launch_bounds__(DEC_THREADS)
         const float pr = __expf(s[g] - mn);
         l[g] = l[g] * corr + pr;
 #pragma unroll
-        for (int j = 0; j < V; ++j) acc[g][j] = fmaf(pr, vv[u][j], acc[g][j] * corr);
+        for (int j = 0; j < V; ++j) acc[g][j] = fmaf(pr, vv[j], acc[g][j] * corr);
         m[g] = mn;
       }
     }
@@ -208,6 +211,8 @@ template <typename T, int HD>
 __global__ void __launch_bounds__(PF_THREADS)
     attn_prefill_kernel(const T *q, const T *kc, const T *vc, const int32_t *bt, const int32_t *seq_lens,
                         T *o, int s_len, int hq, int hkv, int page, int max_blocks, float scale) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ float sm[];
   float *Qs = sm;                         // [BQ][HD]
   float *Ks = Qs + PF_BQ * HD;            // [BK][HD + 1]
@@ -314,9 +319,9 @@ __global__ void __launch_bounds__(PF_THREADS)
 
 static int decode_splits(int batch, int hkv, int max_ctx) {
   const int pairs = batch * hkv;
-  const int target = 2 * 148;
+  const int target = 4 * 148;  // ~4 CTAs per SM keep enough KV bytes in flight
   int s = (target + pairs - 1) / pairs;
-  const int cap = (max_ctx + 127) / 128;
+  const int cap = (max_ctx + 63) / 64;
   s = s < cap ? s : cap;
   return s < 1 ? 1 : s;
 }
@@ -326,7 +331,7 @@ static int launch_decode_g(int G, dim3 grid, const void *q, const void *kc, cons
                            const int32_t *sl, void *o, int hkv, int page, int maxb, float scale, float *ws,
                            int *cnt, cudaStream_t st) {
 #define HX_DEC(GG)                                                                                      \
-  attn_decode_kernel<T, HD, GG><<<grid, DEC_THREADS, 0, st>>>((const T *)q, (const T *)kc, (const T *)vc, bt, \
+  return launch(attn_decode_kernel<T, HD, GG>, dim3(grid), dim3(DEC_THREADS), 0, st, (const T *)q, (const T *)kc, (const T *)vc, bt, \
                                                               sl, (T *)o, hkv, page, maxb, scale, ws, cnt)
   switch (G) {
     case 1: HX_DEC(1); break;
@@ -351,12 +356,14 @@ extern "C" int hx_rope_kv_append(const void *qkv, void *q_out, void *k_cache, vo
   if (!qkv || !q_out || !k_cache || !v_cache || !block_table || !seq_lens || hd % 2 || page_size <= 0)
     return HX_ERR_ARG;
   cudaStream_t st = as_stream(stream);
+  dim3 grid(n_tok, hq + 2 * hkv);
+  const int threads = hd / 2 < 32 ? 32 : hd / 2;
   if (dtype == HX_BF16)
-    rope_append_kernel<<<n_tok, 256, 0, st>>>((const __nv_bfloat16 *)qkv, (__nv_bfloat16 *)q_out,
+    return launch(rope_append_kernel<__nv_bfloat16>, dim3(grid), dim3(threads), 0, st, (const __nv_bfloat16 *)qkv, (__nv_bfloat16 *)q_out,
                                               (__nv_bfloat16 *)k_cache, (__nv_bfloat16 *)v_cache, block_table,
                                               seq_lens, prefill_len, hq, hkv, hd, page_size, max_blocks, theta);
   else
-    rope_append_kernel<<<n_tok, 256, 0, st>>>((const float *)qkv, (float *)q_out, (float *)k_cache,
+    return launch(rope_append_kernel<float>, dim3(grid), dim3(threads), 0, st, (const float *)qkv, (float *)q_out, (float *)k_cache,
                                               (float *)v_cache, block_table, seq_lens, prefill_len, hq, hkv, hd,
                                               page_size, max_blocks, theta);
   return launch_status();
@@ -418,7 +425,7 @@ static int launch_prefill(const void *q, const void *kc, const void *vc, const i
     attr = true;
   }
   dim3 grid((s + PF_BQ - 1) / PF_BQ, hq, batch);
-  attn_prefill_kernel<T, HD><<<grid, PF_THREADS, smem, st>>>((const T *)q, (const T *)kc, (const T *)vc, bt, sl,
+  return launch(attn_prefill_kernel<T, HD>, dim3(grid), dim3(PF_THREADS), smem, st, (const T *)q, (const T *)kc, (const T *)vc, bt, sl,
                                                              (T *)o, s, hq, hkv, page, maxb,
                                                              1.0f / sqrtf((float)HD));
   return launch_status();

@@ -27,6 +27,37 @@ inline int launch_status() {
 
 inline cudaStream_t as_stream(hx_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// ---------------------------------------------------------------- PDL
+// Programmatic dependent launch: every hx kernel triggers its dependents at
+// entry and waits (griddepcontrol.wait) before touching data written by the
+// previous kernel, so a kernel's launch, prologue and -- for the decode GEMM --
+// its first weight-tile loads overlap the previous kernel's tail. Captured
+// into CUDA graphs as programmatic edges.
+extern int g_pdl;
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
+template <typename... KArgs, typename... Args>
+inline int launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                  Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+  ++g_launches;
+  if (e != cudaSuccess) return (int)e;
+  e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : (int)e;
+}
+
 __device__ __forceinline__ float to_f32(float v) { return v; }
 __device__ __forceinline__ float to_f32(__nv_bfloat16 v) { return __bfloat162float(v); }
 template <typename T> __device__ __forceinline__ T from_f32(float v);

@@ -8,11 +8,14 @@
 namespace hx {
 
 unsigned long long g_launches = 0;
+int g_pdl = 1;
 
 constexpr int ROW_THREADS = 256;
 
 template <typename T>
 __global__ void embed_kernel(const int32_t *ids, const T *table, float *x, int hidden, int vocab) {
+  pdl_trigger();
+  pdl_wait();
   const int t = blockIdx.x;
   int id = ids[t];
   id = id < 0 ? 0 : (id >= vocab ? vocab - 1 : id);
@@ -43,23 +46,32 @@ template <typename TO>
 __global__ void __launch_bounds__(ROW_THREADS)
     add_rmsnorm_kernel(float *x, long ldx, const float *delta, const float *gain, TO *out, int hidden,
                        float eps) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float red[32];
   const int t = blockIdx.x;
   float *xr = x + (size_t)t * ldx;
   const float *dr = delta ? delta + (size_t)t * hidden : nullptr;
   constexpr int MAXV = 8;  // hidden <= 8 * 4 * 256 = 8192
-  float v[MAXV][4];
-  float ss = 0.f;
+  float v[MAXV][4], d[MAXV][4], g[MAXV][4];
+  // issue every load (x, delta, gain) before the first use
 #pragma unroll
   for (int r = 0; r < MAXV; ++r) {
     const int i = (r * ROW_THREADS + threadIdx.x) * 4;
     if (i < hidden) {
       Vec16<float>::load(xr + i, v[r]);
-      if (dr) {
-        float d[4];
-        Vec16<float>::load(dr + i, d);
+      if (dr) Vec16<float>::load(dr + i, d[r]);
+      if (out) Vec16<float>::load(gain + i, g[r]);
+    }
+  }
+  float ss = 0.f;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) v[r][j] += d[j];
+  for (int r = 0; r < MAXV; ++r) {
+    const int i = (r * ROW_THREADS + threadIdx.x) * 4;
+    if (i < hidden) {
+      if (dr) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[r][j] += d[r][j];
         Vec16<float>::store(xr + i, v[r]);
       }
 #pragma unroll
@@ -74,16 +86,16 @@ __global__ void __launch_bounds__(ROW_THREADS)
   for (int r = 0; r < MAXV; ++r) {
     const int i = (r * ROW_THREADS + threadIdx.x) * 4;
     if (i < hidden) {
-      float g[4];
-      Vec16<float>::load(gain + i, g);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) o[i + j] = from_f32<TO>((v[r][j] * inv) * g[j]);
+      for (int j = 0; j < 4; ++j) o[i + j] = from_f32<TO>((v[r][j] * inv) * g[r][j]);
     }
   }
 }
 
 template <typename T>
 __global__ void swiglu_kernel(const T *gu, T *out, int inter) {
+  pdl_trigger();
+  pdl_wait();
   const int t = blockIdx.y;
   const T *g = gu + (size_t)t * 2 * inter;
   const T *u = g + inter;
@@ -108,6 +120,8 @@ __device__ __forceinline__ unsigned long long pack_key(float v, int idx) {
 
 __global__ void __launch_bounds__(1024)
     argmax_kernel(const float *logits, long long *keys, int n_cols, int ld, int offset) {
+  pdl_trigger();
+  pdl_wait();
   const int t = blockIdx.x;
   const float *row = logits + (size_t)t * ld;
   float best = -INFINITY;
@@ -136,6 +150,8 @@ __global__ void __launch_bounds__(1024)
 
 __global__ void argmax_finalize_kernel(const long long *keys, int32_t *ids, int32_t *history,
                                        int32_t *step, int s_out, int n_tok, int bump) {
+  pdl_trigger();
+  pdl_wait();
   const int t = threadIdx.x + blockIdx.x * blockDim.x;
   const int st = history ? *step : 0;
   if (t < n_tok) {
@@ -151,6 +167,8 @@ __global__ void argmax_finalize_kernel(const long long *keys, int32_t *ids, int3
 }
 
 __global__ void advance_kernel(int32_t *seq_lens, int batch, int n) {
+  pdl_trigger();
+  pdl_wait();
   const int b = threadIdx.x + blockIdx.x * blockDim.x;
   if (b < batch) seq_lens[b] += n;
 }
@@ -160,6 +178,8 @@ __global__ void advance_kernel(int32_t *seq_lens, int batch, int n) {
 using namespace hx;
 
 extern "C" int hx_version(void) { return 1; }
+
+extern "C" void hx_set_pdl(int enabled) { g_pdl = enabled ? 1 : 0; }
 
 extern "C" uint64_t hx_launch_count(void) { return g_launches; }
 
@@ -180,9 +200,9 @@ extern "C" int hx_embed(const int32_t *ids, const void *table, int table_dtype, 
   if (!ids || !table || !x || hidden % 8) return HX_ERR_ARG;
   cudaStream_t st = as_stream(stream);
   if (table_dtype == HX_BF16)
-    embed_kernel<<<n_tok, 128, 0, st>>>(ids, (const __nv_bfloat16 *)table, x, hidden, vocab);
+    return launch(embed_kernel<__nv_bfloat16>, dim3(n_tok), dim3(128), 0, st, ids, (const __nv_bfloat16 *)table, x, hidden, vocab);
   else
-    embed_kernel<<<n_tok, 128, 0, st>>>(ids, (const float *)table, x, hidden, vocab);
+    return launch(embed_kernel<float>, dim3(n_tok), dim3(128), 0, st, ids, (const float *)table, x, hidden, vocab);
   return launch_status();
 }
 
@@ -193,10 +213,10 @@ static int add_rmsnorm(float *x, long ldx, const float *delta, const float *gain
   if (out && !gain) return HX_ERR_ARG;
   cudaStream_t st = as_stream(stream);
   if (out_dtype == HX_BF16)
-    add_rmsnorm_kernel<__nv_bfloat16><<<n_tok, ROW_THREADS, 0, st>>>(x, ldx, delta, gain, (__nv_bfloat16 *)out,
+    return launch(add_rmsnorm_kernel<__nv_bfloat16>, dim3(n_tok), dim3(ROW_THREADS), 0, st, x, ldx, delta, gain, (__nv_bfloat16 *)out,
                                                                      hidden, eps);
   else
-    add_rmsnorm_kernel<float><<<n_tok, ROW_THREADS, 0, st>>>(x, ldx, delta, gain, (float *)out, hidden, eps);
+    return launch(add_rmsnorm_kernel<float>, dim3(n_tok), dim3(ROW_THREADS), 0, st, x, ldx, delta, gain, (float *)out, hidden, eps);
   return launch_status();
 }
 
@@ -220,16 +240,16 @@ extern "C" int hx_swiglu(const void *gu, void *out, int dtype, int n_tok, int in
   const int V = dtype == HX_BF16 ? 8 : 4;
   dim3 grid((inter / V + 127) / 128, n_tok);
   if (dtype == HX_BF16)
-    swiglu_kernel<<<grid, 128, 0, st>>>((const __nv_bfloat16 *)gu, (__nv_bfloat16 *)out, inter);
+    return launch(swiglu_kernel<__nv_bfloat16>, dim3(grid), dim3(128), 0, st, (const __nv_bfloat16 *)gu, (__nv_bfloat16 *)out, inter);
   else
-    swiglu_kernel<<<grid, 128, 0, st>>>((const float *)gu, (float *)out, inter);
+    return launch(swiglu_kernel<float>, dim3(grid), dim3(128), 0, st, (const float *)gu, (float *)out, inter);
   return launch_status();
 }
 
 extern "C" int hx_advance(int32_t *seq_lens, int batch, int n, hx_stream_t stream) {
   if (batch == 0) return 0;
   if (!seq_lens) return HX_ERR_ARG;
-  advance_kernel<<<(batch + 127) / 128, 128, 0, as_stream(stream)>>>(seq_lens, batch, n);
+  return launch(advance_kernel, dim3((batch + 127) / 128), dim3(128), 0, as_stream(stream), seq_lens, batch, n);
   return launch_status();
 }
 
@@ -237,7 +257,7 @@ extern "C" int hx_argmax_partial(const float *logits, int64_t *keys, int n_tok, 
                                  int vocab_offset, hx_stream_t stream) {
   if (n_tok == 0) return 0;
   if (!logits || !keys || n_cols <= 0 || ld < n_cols) return HX_ERR_ARG;
-  argmax_kernel<<<n_tok, 1024, 0, as_stream(stream)>>>(logits, (long long *)keys, n_cols, ld, vocab_offset);
+  return launch(argmax_kernel, dim3(n_tok), dim3(1024), 0, as_stream(stream), logits, (long long *)keys, n_cols, ld, vocab_offset);
   return launch_status();
 }
 
@@ -245,7 +265,7 @@ extern "C" int hx_argmax_finalize(const int64_t *keys, int32_t *ids, int32_t *hi
                                   int s_out, int n_tok, int bump_step, hx_stream_t stream) {
   if (n_tok == 0) return 0;
   if (!keys || !ids || (history && !step) || n_tok > 1024) return HX_ERR_ARG;
-  argmax_finalize_kernel<<<1, 1024, 0, as_stream(stream)>>>((const long long *)keys, ids, history, step,
+  return launch(argmax_finalize_kernel, dim3(1), dim3(1024), 0, as_stream(stream), (const long long *)keys, ids, history, step,
                                                             s_out, n_tok, bump_step);
   return launch_status();
 }

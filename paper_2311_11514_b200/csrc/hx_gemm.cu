@@ -13,6 +13,11 @@
 //            reduces the fp32 partials in split order (deterministic).
 //   prefill (n_tok > 64):  A = activations (M = 128 tokens), B = weights
 //            (N = 256 features): tensor-bound, one 128x256 fp32 tile in TMEM.
+// Weights may be pre-packed (hx_pack_weight) into [N/128][K/64][128][64]
+// tiles so every 16 KB TMA box is one contiguous HBM stream. Under PDL the
+// producer issues the first STAGES weight tiles before griddepcontrol.wait:
+// weights never depend on the previous kernel, so their HBM latency overlaps
+// the previous kernel's tail.
 // fp32 mode (parity with the CPU oracle) uses a CUDA-core kernel.
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -28,6 +33,7 @@ namespace hx {
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle row
 constexpr int kNumSMs = 148;
+constexpr uint32_t TILE_BYTES = BM * BK * 2;  // one packed 128x64 weight tile
 
 struct GemmArgs {
   void *c;
@@ -38,11 +44,11 @@ struct GemmArgs {
   int kb_total;
   int kb_per_split;
   int a_is_weight;
+  int w_packed;
   float *ws;
   int *counters;
 };
 
-template <int BN>
 __device__ __forceinline__ void store_chunk(const GemmArgs &p, int m, int n0, const float *v) {
   if (m >= p.M) return;
   if (p.c_bf16) {
@@ -89,11 +95,13 @@ __global__ void __launch_bounds__(128, 1)
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(accf + 1);
   __shared__ int s_last;
 
+  pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
   const int split = blockIdx.z, splits = gridDim.z;
   const int kb0 = split * p.kb_per_split;
   const int kb1 = min(p.kb_total, kb0 + p.kb_per_split);
+  const int nkb = kb1 - kb0;
 
   if (threadIdx.x == 0) {
     tma_prefetch(&tm_a);
@@ -114,18 +122,46 @@ __global__ void __launch_bounds__(128, 1)
   if (warp == 0 && lane == 0) {
     // TMA producer
     const uint64_t pol_w = l2_policy_evict_first(), pol_x = l2_policy_evict_last();
-    const uint64_t pol_a = p.a_is_weight ? pol_w : pol_x, pol_b = p.a_is_weight ? pol_x : pol_w;
-    for (int kb = kb0, i = 0; kb < kb1; ++kb, ++i) {
+    // weight operand: A (decode) or B (prefill); packed tiles are row blocks of a [*, 64] tensor
+    auto load_w = [&](uint8_t *dst, int kb) {
+      if (p.a_is_weight) {
+        if (p.w_packed) tma_load_2d(dst, &tm_a, &full[(dst - sa) / A_BYTES], 0, (blockIdx.x * p.kb_total + kb) * BM, pol_w);
+        else tma_load_2d(dst, &tm_a, &full[(dst - sa) / A_BYTES], kb * BK, m0, pol_w);
+      } else {
+        uint64_t *bar = &full[(dst - sb) / B_BYTES];
+        if (p.w_packed) {
+#pragma unroll
+          for (int h = 0; h < BN / BM; ++h)
+            tma_load_2d(dst + h * TILE_BYTES, &tm_b, bar, 0, ((blockIdx.y * (BN / BM) + h) * p.kb_total + kb) * BM, pol_w);
+        } else {
+          tma_load_2d(dst, &tm_b, bar, kb * BK, n0, pol_w);
+        }
+      }
+    };
+    auto load_x = [&](int s, int kb) {
+      if (p.a_is_weight) tma_load_2d(sb + s * B_BYTES, &tm_b, &full[s], kb * BK, n0, pol_x);
+      else tma_load_2d(sa + s * A_BYTES, &tm_a, &full[s], kb * BK, m0, pol_x);
+    };
+    auto wbuf = [&](int s) { return p.a_is_weight ? sa + s * A_BYTES : sb + s * B_BYTES; };
+    // prologue: weight tiles of the first stages go out before the dependency wait
+    const int pre = min(nkb, STAGES);
+    for (int i = 0; i < pre; ++i) {
+      mbar_arrive_expect_tx(&full[i], A_BYTES + B_BYTES);
+      load_w(wbuf(i), kb0 + i);
+    }
+    pdl_wait();
+    for (int i = 0; i < pre; ++i) load_x(i, kb0 + i);
+    for (int i = pre; i < nkb; ++i) {
       const int s = i % STAGES;
       mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
       mbar_arrive_expect_tx(&full[s], A_BYTES + B_BYTES);
-      tma_load_2d(sa + s * A_BYTES, &tm_a, &full[s], kb * BK, m0, pol_a);
-      tma_load_2d(sb + s * B_BYTES, &tm_b, &full[s], kb * BK, n0, pol_b);
+      load_w(wbuf(s), kb0 + i);
+      load_x(s, kb0 + i);
     }
   } else if (warp == 1 && lane == 0) {
     // MMA issuer: 4 x (128 x BN x 16) per 64-wide K block
     constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
-    for (int kb = kb0, i = 0; kb < kb1; ++kb, ++i) {
+    for (int i = 0; i < nkb; ++i) {
       const int s = i % STAGES;
       mbar_wait(&full[s], (i / STAGES) & 1);
       tc_fence_after();
@@ -151,7 +187,7 @@ __global__ void __launch_bounds__(128, 1)
     for (int c = 0; c < BN; c += 16) {
       float v[16];
       tmem_ld16(trow + c, v);
-      store_chunk<BN>(p, m, n0 + c, v);
+      store_chunk(p, m, n0 + c, v);
     }
   } else {
     const int tile = blockIdx.y * gridDim.x + blockIdx.x;
@@ -161,7 +197,8 @@ __global__ void __launch_bounds__(128, 1)
       float v[16];
       tmem_ld16(trow + c, v);
 #pragma unroll
-      for (int j = 0; j < 16; j += 4) __stcg(reinterpret_cast<float4 *>(mine + c + j), make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
+      for (int j = 0; j < 16; j += 4)
+        __stcg(reinterpret_cast<float4 *>(mine + c + j), make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
     }
     __threadfence();
     __syncthreads();
@@ -187,7 +224,7 @@ __global__ void __launch_bounds__(128, 1)
             acc[j] += f.x; acc[j + 1] += f.y; acc[j + 2] += f.z; acc[j + 3] += f.w;
           }
         }
-        store_chunk<BN>(p, m, n0 + c, acc);
+        store_chunk(p, m, n0 + c, acc);
       }
     }
   }
@@ -196,11 +233,36 @@ __global__ void __launch_bounds__(128, 1)
   if (warp == 1) tmem_dealloc(tmem, TMEM_COLS);
 }
 
+// ------------------------------------------------------------------ packing
+// dst[(t * KB + kb) * 128 * 64 + r * 64 + c] = src[(t * 128 + r) * K + kb * 64 + c] (0 if OOB)
+__global__ void pack_weight_kernel(const __nv_bfloat16 *__restrict__ src, __nv_bfloat16 *__restrict__ dst,
+                                   int N, int K, int KB) {
+  pdl_trigger();
+  pdl_wait();
+  const size_t tile = blockIdx.x;  // t * KB + kb
+  const int t = (int)(tile / KB), kb = (int)(tile % KB);
+  for (int e = threadIdx.x * 8; e < BM * BK; e += blockDim.x * 8) {
+    const int r = e / BK, c = e % BK;
+    const int n = t * BM + r, k = kb * BK + c;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (n < N && k + 8 <= K) {
+      v = *reinterpret_cast<const uint4 *>(src + (size_t)n * K + k);
+    } else if (n < N) {
+      __nv_bfloat16 tmp[8];
+      for (int j = 0; j < 8; ++j) tmp[j] = k + j < K ? src[(size_t)n * K + k + j] : __float2bfloat16_rn(0.f);
+      v = *reinterpret_cast<uint4 *>(tmp);
+    }
+    *reinterpret_cast<uint4 *>(dst + tile * BM * BK + e) = v;
+  }
+}
+
 // ------------------------------------------------------------------ fp32 SIMT
 // Y[t, n] = sum_k X[t, k] W[n, k]; 64x64 tile, 256 threads x (4x4).
 __global__ void __launch_bounds__(256)
     gemm_f32_simt_kernel(const float *__restrict__ w, const float *__restrict__ x, float *y,
                          int n_tok, int n_out, int K, int ldy, int accumulate) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float xs[16][64 + 4];
   __shared__ float ws[16][64 + 4];
   const int t0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
@@ -261,7 +323,7 @@ static int get_encode() {
 
 // 2-D bf16 tensor [rows, cols] row-major with row pitch `pitch` elements;
 // box = box_rows x 64 columns, 128B swizzle.
-static int make_map(CUtensorMap *map, const void *ptr, int rows, int cols, long pitch, int box_rows) {
+static int make_map(CUtensorMap *map, const void *ptr, long rows, int cols, long pitch, int box_rows) {
   if (get_encode()) return HX_ERR_DRIVER;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)pitch * 2};
@@ -289,8 +351,7 @@ static int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, const GemmArg
     attr_done = true;
   }
   dim3 grid((p.M + BM - 1) / BM, (p.N + BN - 1) / BN, splits);
-  gemm_bf16_tc_kernel<BN, STAGES><<<grid, 128, smem, st>>>(ma, mb, p);
-  return launch_status();
+  return launch(gemm_bf16_tc_kernel<BN, STAGES>, grid, dim3(128), smem, st, ma, mb, p);
 }
 
 struct Plan {
@@ -341,9 +402,19 @@ extern "C" size_t hx_linear_workspace(int dtype, int n_tok, int n_out, int k_dim
   if (dtype != HX_BF16) return 0;
   Plan pl = plan_gemm(n_tok, n_out, k_dim);
   if (pl.splits <= 1) return 0;
-  // fp32 partials + one ticket counter per tile (counters first, 256-aligned)
-  const size_t counters = kTicketBytes;
-  return counters + (size_t)pl.tiles * pl.splits * BM * pl.bn * sizeof(float);
+  return kTicketBytes + (size_t)pl.tiles * pl.splits * BM * pl.bn * sizeof(float);
+}
+
+extern "C" size_t hx_packed_weight_elems(int n_out, int k_dim) {
+  return (size_t)((n_out + BM - 1) / BM) * ((k_dim + BK - 1) / BK) * BM * BK;
+}
+
+extern "C" int hx_pack_weight(const void *w, void *packed, int n_out, int k_dim, hx_stream_t stream) {
+  if (!w || !packed || n_out <= 0 || k_dim <= 0 || k_dim % 8) return HX_ERR_ARG;
+  const int KB = (k_dim + BK - 1) / BK;
+  const int tiles = ((n_out + BM - 1) / BM) * KB;
+  return launch(pack_weight_kernel, dim3(tiles), dim3(256), 0, as_stream(stream), (const __nv_bfloat16 *)w,
+                (__nv_bfloat16 *)packed, n_out, k_dim, KB);
 }
 
 extern "C" int hx_linear(const void *w, const void *x, void *y, int dtype, int y_dtype, int n_tok,
@@ -351,14 +422,14 @@ extern "C" int hx_linear(const void *w, const void *x, void *y, int dtype, int y
                          size_t workspace_bytes, hx_stream_t stream) {
   if (n_tok <= 0 || n_out <= 0 || k_dim <= 0) return n_tok == 0 ? 0 : HX_ERR_ARG;
   if (!w || !x || !y || ldy < n_out) return HX_ERR_ARG;
-  const int accumulate = flags & 1;
+  const int accumulate = flags & HX_LINEAR_ACCUMULATE;
+  const int packed = (flags & HX_LINEAR_PACKED) ? 1 : 0;
   cudaStream_t st = as_stream(stream);
   if (dtype == HX_F32) {
-    if (y_dtype != HX_F32) return HX_ERR_UNSUPPORTED;
+    if (y_dtype != HX_F32 || packed) return HX_ERR_UNSUPPORTED;
     dim3 grid((n_out + 63) / 64, (n_tok + 63) / 64);
-    gemm_f32_simt_kernel<<<grid, 256, 0, st>>>((const float *)w, (const float *)x, (float *)y, n_tok,
-                                                n_out, k_dim, ldy, accumulate);
-    return launch_status();
+    return launch(gemm_f32_simt_kernel, grid, dim3(256), 0, st, (const float *)w, (const float *)x, (float *)y,
+                  n_tok, n_out, k_dim, ldy, accumulate);
   }
   if (dtype != HX_BF16) return HX_ERR_ARG;
   if (k_dim % 8) return HX_ERR_UNSUPPORTED;  // TMA row pitch must be 16B aligned
@@ -371,24 +442,27 @@ extern "C" int hx_linear(const void *w, const void *x, void *y, int dtype, int y
   p.accumulate = accumulate;
   p.kb_total = (k_dim + BK - 1) / BK;
   p.kb_per_split = pl.kb_per;
+  p.w_packed = packed;
   CUtensorMap ma, mb;
   int rc;
+  const long packed_rows = (long)((n_out + BM - 1) / BM) * p.kb_total * BM;
   if (pl.decode) {
     p.M = n_out; p.N = n_tok; p.ldm = 1; p.ldn = ldy; p.a_is_weight = 1;
-    if ((rc = make_map(&ma, w, n_out, k_dim, k_dim, BM))) return rc;
+    rc = packed ? make_map(&ma, w, packed_rows, BK, BK, BM) : make_map(&ma, w, n_out, k_dim, k_dim, BM);
+    if (rc) return rc;
     if ((rc = make_map(&mb, x, n_tok, k_dim, k_dim, pl.bn))) return rc;
   } else {
     p.M = n_tok; p.N = n_out; p.ldm = ldy; p.ldn = 1; p.a_is_weight = 0;
     if ((rc = make_map(&ma, x, n_tok, k_dim, k_dim, BM))) return rc;
-    if ((rc = make_map(&mb, w, n_out, k_dim, k_dim, pl.bn))) return rc;
+    rc = packed ? make_map(&mb, w, packed_rows, BK, BK, BM) : make_map(&mb, w, n_out, k_dim, k_dim, pl.bn);
+    if (rc) return rc;
   }
   if (pl.splits > 1) {
     const size_t need = hx_linear_workspace(dtype, n_tok, n_out, k_dim);
     if (!workspace || workspace_bytes < need) return HX_ERR_WORKSPACE;
     if (pl.tiles > kMaxTickets) return HX_ERR_UNSUPPORTED;
-    const size_t counters = kTicketBytes;
     p.counters = reinterpret_cast<int *>(workspace);
-    p.ws = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(workspace) + counters);
+    p.ws = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(workspace) + kTicketBytes);
   }
   switch (pl.bn) {
     case 16: return launch_tc<16, 6>(ma, mb, p, pl.splits, st);

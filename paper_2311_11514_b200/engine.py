@@ -152,10 +152,19 @@ class RankExecutor:
     """One (stage, TP rank) of the pipeline: weights, KV pages, buffers, kernels."""
 
     def __init__(self, cfg: LlamaConfig, role: Role, dtype: torch.dtype, batch: int, max_prompt: int,
-                 max_out: int, device, weights: dict, kernels=None, page_size: int = 64):
+                 max_out: int, device, weights: dict, kernels=None, page_size: int = 64,
+                 pack_weights: bool = True):
         self.cfg, self.role, self.dtype, self.device = cfg, role, dtype, torch.device(device)
         self.k = kernels or _ops
         self.w = weights
+        if pack_weights and dtype == torch.bfloat16 and self.device.type == "cuda":
+            # tile-contiguous layout for the weight-streaming GEMM (hx_pack_weight)
+            for lw in weights["layers"]:
+                for name in ("wqkv", "wo", "wgu", "wdown"):
+                    lw[name] = _ops.PackedWeight(lw[name])
+            if "lm_head" in weights:
+                weights["lm_head"] = _ops.PackedWeight(weights["lm_head"])
+            torch.cuda.synchronize(self.device)
         tp = role.tp
         self.hq, self.hkv = cfg.num_heads // tp, cfg.num_kv_heads // tp
         self.hd = cfg.head_dim
@@ -324,7 +333,7 @@ class Engine:
     def __init__(self, plan: GlobalAssignment, cfg: LlamaConfig, *, dtype: str = "bf16",
                  batch: int, max_prompt: int, max_out: int, pipeline: int = 0, comm: str = "local",
                  device=None, seed: int = 0, weights: str = "host", page_size: int = 64,
-                 use_graphs: bool = True, kernels=None):
+                 use_graphs: bool = True, kernels=None, pack_weights: bool = True):
         if dtype not in DTYPES:
             raise InputError(f"dtype must be one of {sorted(DTYPES)}")
         self.plan, self.cfg, self.dtype = plan, cfg, DTYPES[dtype]
@@ -349,7 +358,8 @@ class Engine:
             _ops.load()
         execs = [RankExecutor(cfg, r, self.dtype, batch, max_prompt, max_out, self.device,
                               load_rank_weights(cfg, r, self.dtype, self.device, seed, weights),
-                              kernels=self.kernels, page_size=page_size) for r in local]
+                              kernels=self.kernels, page_size=page_size,
+                              pack_weights=pack_weights and kernels is None) for r in local]
         self.drivers = []
         for j in sorted({r.stage for r in local}):
             self.drivers.append(StageDriver([e for e in execs if e.role.stage == j], self.comm, j))

@@ -32,6 +32,9 @@ _SIGS = {
     "hx_residual_add_rmsnorm": ([_P, _P, _P, _P, _I, _I, _I, _F, _P], _I),
     "hx_linear": ([_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _SZ, _P], _I),
     "hx_linear_workspace": ([_I, _I, _I, _I], _SZ),
+    "hx_pack_weight": ([_P, _P, _I, _I, _P], _I),
+    "hx_packed_weight_elems": ([_I, _I], _SZ),
+    "hx_set_pdl": ([_I], None),
     "hx_swiglu": ([_P, _P, _I, _I, _I, _P], _I),
     "hx_rope_kv_append": ([_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _F, _P], _I),
     "hx_attn_decode_paged": ([_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _SZ, _P], _I),
@@ -117,12 +120,47 @@ def linear_workspace(dtype, n_tok, n_out, k_dim) -> int:
     return int(load().hx_linear_workspace(dtype_code(dtype), n_tok, n_out, k_dim))
 
 
+HX_LINEAR_ACCUMULATE, HX_LINEAR_PACKED = 1, 2
+
+
+class PackedWeight:
+    """A bf16 [n_out, k] weight held in the hx_pack_weight tile layout
+    ([n/128][k/64][128][64], zero padded): each 16 KB tile the decode GEMM
+    streams is one contiguous HBM range."""
+
+    def __init__(self, w: torch.Tensor):
+        if w.dtype != torch.bfloat16 or w.dim() != 2:
+            raise HxError("PackedWeight needs a 2-D bf16 tensor")
+        self.shape = tuple(w.shape)
+        self.dtype = w.dtype
+        n, k = self.shape
+        self.data = torch.empty(int(load().hx_packed_weight_elems(n, k)), dtype=w.dtype, device=w.device)
+        _check(load().hx_pack_weight(_p(w.contiguous()), _p(self.data), n, k, _stream()), "hx_pack_weight")
+
+    def numel(self):
+        return self.shape[0] * self.shape[1]
+
+    def element_size(self):
+        return 2
+
+
+def set_pdl(enabled: bool):
+    load().hx_set_pdl(1 if enabled else 0)
+
+
 def linear(w, x, y, n_tok, workspace=None, accumulate=False):
-    """y[:n_tok, :n_out] (+)= x[:n_tok] @ w.T ; w [n_out, K] row-major."""
+    """y[:n_tok, :n_out] (+)= x[:n_tok] @ w.T ; w [n_out, K] row-major tensor
+    or a PackedWeight."""
     n_out, k = w.shape
+    flags = HX_LINEAR_ACCUMULATE if accumulate else 0
+    if isinstance(w, PackedWeight):
+        flags |= HX_LINEAR_PACKED
+        wp = w.data
+    else:
+        wp = w
     ws = workspace
-    _check(load().hx_linear(_p(w), _p(x), _p(y), dtype_code(w.dtype), dtype_code(y.dtype), n_tok,
-                            n_out, k, y.shape[-1], 1 if accumulate else 0, _p(ws),
+    _check(load().hx_linear(_p(wp), _p(x), _p(y), dtype_code(w.dtype), dtype_code(y.dtype), n_tok,
+                            n_out, k, y.shape[-1], flags, _p(ws),
                             0 if ws is None else ws.numel() * ws.element_size(), _stream()),
            "hx_linear")
 

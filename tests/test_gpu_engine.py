@@ -51,24 +51,32 @@ def test_tiny_fp32_graph_replay_same_ids():
     assert len(a.step_ms) == 15
 
 
+BF16_TOL_EMULATED = 5e-3   # vs the oracle that rounds activations where the engine does
+BF16_TOL_FP32ACT = 3e-2    # vs the fp32-activation oracle on the same bf16 weights
+
+
 def _bf16_check(cfg, tps, layers, b, s, s_out, page=64):
-    w = init_host_weights(cfg, 0)
+    w = bf16_weights(init_host_weights(cfg, 0))
     prompt = synthetic_prompts(cfg, b, s, seed=1)
-    oracle = Oracle(cfg, bf16_weights(w))
-    ids_o, lg_o = oracle.generate(prompt, s_out)
+    ids_o, lg_o = Oracle(cfg, w, act_bf16=True).generate(prompt, s_out)
     eng = Engine(simple_plan(tps, layers), cfg, dtype="bf16", batch=b, max_prompt=s, max_out=s_out,
                  device="cuda:0", page_size=page)
     r = eng.generate(prompt, s_out, forced=ids_o)
     scale = np.abs(lg_o).max(axis=-1, keepdims=True)
     err = np.abs(r.logits - lg_o) / scale
-    assert err.max() < 2e-2, err.max()
+    _, lg_f = Oracle(cfg, w).generate(prompt, s_out, forced=ids_o)
+    err_f = np.abs(r.logits - lg_f) / np.abs(lg_f).max(axis=-1, keepdims=True)
+    print(f"bf16 teacher-forced max rel logit err: {err.max():.2e} (emulated), {err_f.max():.2e} (fp32 act)")
+    assert err.max() < BF16_TOL_EMULATED, err.max()
+    assert err_f.max() < BF16_TOL_FP32ACT, err_f.max()
     srt = np.sort(lg_o, -1)
     margin = (srt[..., -1] - srt[..., -2]) / scale[..., 0]
     ok = margin > 2 * err.max()
     agree = (r.ids.T == ids_o.T)[ok]
     assert agree.mean() >= 0.99
+    # free-running: identical to the teacher-forced run up to its first divergence
     free = eng.generate(prompt, s_out)
-    assert np.array_equal(free.ids, r.ids) or free.ids[:, 0].tolist() == ids_o[:, 0].tolist()
+    assert np.array_equal(free.ids[:, 0], r.ids[:, 0])
     return err.max()
 
 

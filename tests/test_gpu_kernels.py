@@ -33,13 +33,15 @@ PREFILL_SHAPES = [(4096, 12288, 4096), (4096, 4096, 11008), (300, 768, 256), (13
 
 @pytest.mark.parametrize("n_tok,n_out,k", DECODE_SHAPES + PREFILL_SHAPES)
 @pytest.mark.parametrize("ydt", [torch.float32, torch.bfloat16])
-def test_linear_bf16(n_tok, n_out, k, ydt):
+@pytest.mark.parametrize("packed", [False, True])
+def test_linear_bf16(n_tok, n_out, k, ydt, packed):
     g = torch.Generator(device=DEV).manual_seed(n_tok * 7 + n_out + k)
     w = (torch.randn(n_out, k, device=DEV, generator=g) * 0.02).bfloat16()
     x = torch.randn(n_tok, k, device=DEV, generator=g).bfloat16()
     y = torch.full((n_tok, n_out), float("nan"), device=DEV, dtype=ydt)
     ws = torch.zeros(ops.linear_workspace(torch.bfloat16, n_tok, n_out, k) // 4 + 64, dtype=torch.int32, device=DEV)
-    ops.linear(w, x, y, n_tok, ws)
+    wl = ops.PackedWeight(w) if packed else w
+    ops.linear(wl, x, y, n_tok, ws)
     torch.cuda.synchronize()
     want = x.float() @ w.float().T
     tol = 2e-5 * math.sqrt(k) if ydt == torch.float32 else 8e-3
@@ -47,7 +49,7 @@ def test_linear_bf16(n_tok, n_out, k, ydt):
     assert rel_err(y, want) < tol
     # ticket counters are re-armed: a second launch gives identical bits
     y2 = torch.empty_like(y)
-    ops.linear(w, x, y2, n_tok, ws)
+    ops.linear(wl, x, y2, n_tok, ws)
     torch.cuda.synchronize()
     assert torch.equal(y, y2)
 
@@ -67,6 +69,32 @@ def test_linear_shared_workspace_across_shapes():
             torch.cuda.synchronize()
             assert rel_err(y[:n_tok], x[:n_tok].float() @ w.float().T) < 1e-3
             assert not y[n_tok:].any()
+
+
+def test_pack_weight_layout():
+    w = torch.randn(300, 200, device=DEV).bfloat16()   # ragged in both dims -> zero padding
+    pw = ops.PackedWeight(w)
+    torch.cuda.synchronize()
+    t = pw.data.view(3, 4, 128, 64)
+    pad = torch.zeros(384, 256, device=DEV, dtype=torch.bfloat16)
+    pad[:300, :200] = w
+    want = pad.view(3, 128, 4, 64).permute(0, 2, 1, 3)
+    assert torch.equal(t, want)
+
+
+def test_pdl_off_gives_identical_bits():
+    w = ops.PackedWeight((torch.randn(4096, 4096, device=DEV) * 0.02).bfloat16())
+    x = torch.randn(8, 4096, device=DEV).bfloat16()
+    ws = torch.zeros(ops.linear_workspace(torch.bfloat16, 8, 4096, 4096) // 4 + 64, dtype=torch.int32, device=DEV)
+    y1, y2 = torch.empty(8, 4096, device=DEV), torch.empty(8, 4096, device=DEV)
+    ops.linear(w, x, y1, 8, ws)
+    ops.set_pdl(False)
+    try:
+        ops.linear(w, x, y2, 8, ws)
+    finally:
+        ops.set_pdl(True)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2)
 
 
 def test_linear_bf16_accumulate_and_pitch():
