@@ -233,6 +233,204 @@ __global__ void __launch_bounds__(128, 1)
   if (warp == 1) tmem_dealloc(tmem, TMEM_COLS);
 }
 
+// ------------------------------------------------------------------ stream-K decode
+// Persistent weight-streaming GEMM for decode (A = weights, 128-row tiles;
+// B = the n_tok <= 64 activation rows). The tiles x K-blocks unit space is
+// cut into one contiguous, equal range per CTA (2 CTAs/SM), so every CTA
+// streams the same number of 16 KB weight tiles with one uninterrupted TMA
+// pipeline across tile boundaries -- no wave quantisation, no per-tile
+// pipeline refill. Warp roles: 0 = TMA producer, 1 = MMA issuer (TMEM
+// accumulator double-buffered across segments), 2..5 = epilogue. A segment
+// covering a whole tile stores straight to C; partial segments (at most the
+// first and last of each CTA) go to a workspace slot, and the tile's last
+// contributor (atomic ticket) sums the slots in CTA order (deterministic).
+struct SKArgs {
+  void *c;
+  long ldm, ldn;
+  int M, N;
+  int c_bf16, accumulate, w_packed;
+  int KB, units;
+  float *ws;
+  int *counters;
+};
+
+__device__ __forceinline__ int sk_start(int c, int units, int G) { return (int)((long)c * units / G); }
+
+// first CTA whose range contains unit u
+__device__ __forceinline__ int sk_owner(int u, int units, int G) {
+  int c = (int)((long)u * G / units);
+  while (c + 1 < G && sk_start(c + 1, units, G) <= u) ++c;
+  while (c > 0 && sk_start(c, units, G) > u) --c;
+  return c;
+}
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(192, 2)
+    gemm_streamk_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
+                        SKArgs p) {
+  constexpr uint32_t A_BYTES = BM * BK * 2;
+  constexpr uint32_t B_BYTES = BN * BK * 2;
+  constexpr uint32_t TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : 128);
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *sa = smem;
+  uint8_t *sb = smem + STAGES * A_BYTES;
+  uint64_t *full = reinterpret_cast<uint64_t *>(sb + STAGES * B_BYTES);
+  uint64_t *empty = full + STAGES;
+  uint64_t *tfull = empty + STAGES;   // [2]
+  uint64_t *tempty = tfull + 2;       // [2]
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+  __shared__ int s_last;
+
+  pdl_trigger();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = gridDim.x, c = blockIdx.x;
+  const int u0 = sk_start(c, p.units, G), u1 = sk_start(c + 1, p.units, G);
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tm_w);
+    tma_prefetch(&tm_x);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol_w = l2_policy_evict_first(), pol_x = l2_policy_evict_last();
+      auto load_w = [&](int s, int u) {
+        const int t = u / p.KB, kb = u % p.KB;
+        if (p.w_packed) tma_load_2d(sa + s * A_BYTES, &tm_w, &full[s], 0, u * BM, pol_w);
+        else tma_load_2d(sa + s * A_BYTES, &tm_w, &full[s], kb * BK, t * BM, pol_w);
+      };
+      auto load_x = [&](int s, int u) { tma_load_2d(sb + s * B_BYTES, &tm_x, &full[s], (u % p.KB) * BK, 0, pol_x); };
+      const int n = u1 - u0;
+      const int pre = min(n, STAGES);
+      for (int i = 0; i < pre; ++i) {  // weights first: they do not depend on the previous kernel
+        mbar_arrive_expect_tx(&full[i], A_BYTES + B_BYTES);
+        load_w(i, u0 + i);
+      }
+      pdl_wait();
+      for (int i = 0; i < pre; ++i) load_x(i, u0 + i);
+      for (int i = pre; i < n; ++i) {
+        const int s = i % STAGES;
+        mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full[s], A_BYTES + B_BYTES);
+        load_w(s, u0 + i);
+        load_x(s, u0 + i);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+      int i = 0, seg = 0;
+      for (int u = u0; u < u1; ++seg) {
+        const int t = u / p.KB;
+        const int ue = min(u1, (t + 1) * p.KB);
+        const int buf = seg & 1;
+        mbar_wait(&tempty[buf], ((seg >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t acc = tmem + buf * BN;
+        for (int first = 1; u < ue; ++u, ++i, first = 0) {
+          const int s = i % STAGES;
+          mbar_wait(&full[s], (i / STAGES) & 1);
+          tc_fence_after();
+          const uint64_t ad = umma_desc_sw128(sa + s * A_BYTES);
+          const uint64_t bd = umma_desc_sw128(sb + s * B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk)
+            umma_bf16(acc, ad + 2 * kk, bd + 2 * kk, idesc, (first && kk == 0) ? 0u : 1u);
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&tfull[buf]);
+      }
+    }
+  } else {
+    // epilogue warps 2..5 -> TMEM lane quarters (warp % 4)
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const int etid = threadIdx.x - 64;  // 0..127
+    int seg = 0;
+    for (int u = u0; u < u1; ++seg) {
+      const int t = u / p.KB;
+      const int kb_lo = u - t * p.KB;
+      const int ue = min(u1, (t + 1) * p.KB);
+      const int kb_hi = ue - t * p.KB;
+      u = ue;
+      const int buf = seg & 1;
+      mbar_wait(&tfull[buf], (seg >> 1) & 1);
+      tc_fence_after();
+      const uint32_t tacc = tmem + ((uint32_t)(q * 32) << 16) + buf * BN;
+      const int m = t * BM + row;
+      GemmArgs ga{};
+      ga.c = p.c; ga.ldm = p.ldm; ga.ldn = p.ldn; ga.M = p.M; ga.N = p.N;
+      ga.c_bf16 = p.c_bf16; ga.accumulate = p.accumulate;
+      const bool whole = (kb_lo == 0 && kb_hi == p.KB);
+      // partial tile: slot 2c (this CTA's first segment) or 2c+1 (its last)
+      float *mine = p.ws + ((size_t)(2 * c + (seg == 0 ? 0 : 1)) * BM + row) * BN;
+#pragma unroll 1
+      for (int cc = 0; cc < BN; cc += 16) {
+        float v[16];
+        tmem_ld16(tacc + cc, v);
+        if (whole) {
+          store_chunk(ga, m, cc, v);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; j += 4)
+            __stcg(reinterpret_cast<float4 *>(mine + cc + j), make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[buf]);
+      if (whole) continue;
+      __threadfence();
+      named_bar_sync(1, 128);
+      const int c_first = sk_owner(t * p.KB, p.units, G);
+      const int c_last = sk_owner((t + 1) * p.KB - 1, p.units, G);
+      if (etid == 0) {
+        const int tk = atomicAdd(&p.counters[t], 1);
+        s_last = (tk == c_last - c_first);
+        if (s_last) p.counters[t] = 0;
+      }
+      named_bar_sync(1, 128);
+      if (s_last) {
+        __threadfence();
+#pragma unroll 1
+        for (int ch = 0; ch < BN; ch += 16) {
+          float acc[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+          for (int cc = c_first; cc <= c_last; ++cc) {
+            // tile t is the first segment of cc unless cc started before the tile
+            const int sl = 2 * cc + (sk_start(cc, p.units, G) < t * p.KB ? 1 : 0);
+            const float *src = p.ws + ((size_t)sl * BM + row) * BN + ch;
+#pragma unroll
+            for (int j = 0; j < 16; j += 4) {
+              const float4 f = __ldcg(reinterpret_cast<const float4 *>(src + j));
+              acc[j] += f.x; acc[j + 1] += f.y; acc[j + 2] += f.z; acc[j + 3] += f.w;
+            }
+          }
+          store_chunk(ga, m, ch, acc);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, TMEM_COLS);
+}
+
 // ------------------------------------------------------------------ packing
 // dst[(t * KB + kb) * 128 * 64 + r * 64 + c] = src[(t * 128 + r) * K + kb * 64 + c] (0 if OOB)
 __global__ void pack_weight_kernel(const __nv_bfloat16 *__restrict__ src, __nv_bfloat16 *__restrict__ dst,
@@ -398,11 +596,28 @@ static Plan plan_gemm(int n_tok, int n_out, int K) {
 
 using namespace hx;
 
+static int sk_grid(int units) { return std::min(units, 2 * kNumSMs); }
+
 extern "C" size_t hx_linear_workspace(int dtype, int n_tok, int n_out, int k_dim) {
   if (dtype != HX_BF16) return 0;
   Plan pl = plan_gemm(n_tok, n_out, k_dim);
+  if (pl.decode) {  // stream-K: two partial slots per CTA
+    const int units = pl.tiles * ((k_dim + BK - 1) / BK);
+    return kTicketBytes + (size_t)2 * sk_grid(units) * BM * pl.bn * sizeof(float);
+  }
   if (pl.splits <= 1) return 0;
   return kTicketBytes + (size_t)pl.tiles * pl.splits * BM * pl.bn * sizeof(float);
+}
+
+template <int BN, int STAGES>
+static int launch_sk(const CUtensorMap &mw, const CUtensorMap &mx, const SKArgs &p, cudaStream_t st) {
+  const size_t smem = 1024 + STAGES * (BM * BK * 2 + BN * BK * 2) + (2 * STAGES + 4) * 8 + 16;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaFuncSetAttribute(gemm_streamk_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_done = true;
+  }
+  return launch(gemm_streamk_kernel<BN, STAGES>, dim3(sk_grid(p.units)), dim3(192), smem, st, mw, mx, p);
 }
 
 extern "C" size_t hx_packed_weight_elems(int n_out, int k_dim) {
@@ -447,10 +662,23 @@ extern "C" int hx_linear(const void *w, const void *x, void *y, int dtype, int y
   int rc;
   const long packed_rows = (long)((n_out + BM - 1) / BM) * p.kb_total * BM;
   if (pl.decode) {
-    p.M = n_out; p.N = n_tok; p.ldm = 1; p.ldn = ldy; p.a_is_weight = 1;
     rc = packed ? make_map(&ma, w, packed_rows, BK, BK, BM) : make_map(&ma, w, n_out, k_dim, k_dim, BM);
     if (rc) return rc;
     if ((rc = make_map(&mb, x, n_tok, k_dim, k_dim, pl.bn))) return rc;
+    SKArgs sk{};
+    sk.c = y; sk.ldm = 1; sk.ldn = ldy; sk.M = n_out; sk.N = n_tok;
+    sk.c_bf16 = p.c_bf16; sk.accumulate = accumulate; sk.w_packed = packed;
+    sk.KB = p.kb_total; sk.units = pl.tiles * p.kb_total;
+    const size_t need = hx_linear_workspace(dtype, n_tok, n_out, k_dim);
+    if (!workspace || workspace_bytes < need) return HX_ERR_WORKSPACE;
+    if (pl.tiles > kMaxTickets) return HX_ERR_UNSUPPORTED;
+    sk.counters = reinterpret_cast<int *>(workspace);
+    sk.ws = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(workspace) + kTicketBytes);
+    switch (pl.bn) {
+      case 16: return launch_sk<16, 6>(ma, mb, sk, st);
+      case 32: return launch_sk<32, 5>(ma, mb, sk, st);
+      default: return launch_sk<64, 4>(ma, mb, sk, st);
+    }
   } else {
     p.M = n_tok; p.N = n_out; p.ldm = ldy; p.ldn = 1; p.a_is_weight = 0;
     if ((rc = make_map(&ma, x, n_tok, k_dim, k_dim, BM))) return rc;
