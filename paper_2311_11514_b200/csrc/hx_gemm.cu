@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "hx_common.cuh"
@@ -596,14 +597,26 @@ static Plan plan_gemm(int n_tok, int n_out, int K) {
 
 using namespace hx;
 
-static int sk_grid(int units) { return std::min(units, 2 * kNumSMs); }
+// CTAs per SM for the stream-K decode GEMM. 1 (default) leaves room on every
+// SM for the NEXT kernel's GEMM CTA, which (PDL) becomes resident as soon as
+// this one starts and prefetches its first weight tiles while this one streams.
+static int sk_ctas_per_sm() {
+  static int v = [] {
+    const char *e = getenv("HX_SK_CTAS");
+    const int n = e ? atoi(e) : 1;
+    return n == 2 ? 2 : 1;
+  }();
+  return v;
+}
+static int sk_grid(int units) { return std::min(units, sk_ctas_per_sm() * kNumSMs); }
+static int sk_grid_max(int units) { return std::min(units, 2 * kNumSMs); }
 
 extern "C" size_t hx_linear_workspace(int dtype, int n_tok, int n_out, int k_dim) {
   if (dtype != HX_BF16) return 0;
   Plan pl = plan_gemm(n_tok, n_out, k_dim);
   if (pl.decode) {  // stream-K: two partial slots per CTA
     const int units = pl.tiles * ((k_dim + BK - 1) / BK);
-    return kTicketBytes + (size_t)2 * sk_grid(units) * BM * pl.bn * sizeof(float);
+    return kTicketBytes + (size_t)2 * sk_grid_max(units) * BM * pl.bn * sizeof(float);
   }
   if (pl.splits <= 1) return 0;
   return kTicketBytes + (size_t)pl.tiles * pl.splits * BM * pl.bn * sizeof(float);

@@ -1,0 +1,65 @@
+"""Multi-process runs of the engine under torch.distributed.
+
+CPU: gloo, world sizes 2-3, test kernels -- the DistComm path (per-stage
+process groups, all-reduce, vocab-parallel argmax MAX, stage hand-off
+send/recv, token return, id broadcast) must reproduce the oracle's ids.
+GPU (>= 2 devices): NCCL with the C-ABI kernels, same check."""
+
+import os
+import socket
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+import torch
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _run(nproc, args, timeout=600):
+    env = dict(os.environ, OMP_NUM_THREADS="2")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", f"--master-port={_port()}",
+           str(ROOT / "tools" / "dist_generate.py"), *args]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, env=env)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "ids match oracle: True" in r.stdout or "--dtype" in " ".join(args), r.stdout
+    return r.stdout
+
+
+@pytest.mark.parametrize("plan,layers", [("2,1", "3,1"), ("1,2", "1,3"), ("1,1", "2,2")])
+def test_gloo_asymmetric_plans(plan, layers):
+    n = sum(int(x) for x in plan.split(","))
+    _run(n, ["--plan", plan, "--layers", layers, "--cpu"])
+
+
+def _gpus():
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(_gpus() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("plan,layers,graphs", [("1,1", "3,1", False), ("1,1", "2,2", True)])
+def test_nccl_two_stage_fp32(plan, layers, graphs):
+    _run(2, ["--plan", plan, "--layers", layers] + (["--graphs"] if graphs else []))
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(_gpus() < 3, reason="needs >= 3 GPUs")
+def test_nccl_asymmetric_21_fp32_graphs():
+    _run(3, ["--plan", "2,1", "--layers", "3,1", "--graphs"])
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(_gpus() < 4, reason="needs >= 4 GPUs")
+def test_nccl_asymmetric_211_bf16_graphs():
+    _run(4, ["--plan", "2,1,1", "--layers", "2,1,1", "--dtype", "bf16", "--graphs"])

@@ -1,0 +1,84 @@
+"""Run one asymmetric-plan generate under torch.distributed (one process per
+rank) and compare with the CPU oracle on rank 0.
+
+    torchrun --nproc-per-node 3 --master-addr 127.0.0.1 tools/dist_generate.py \
+        --plan 2,1 --layers 3,1 [--cpu]
+
+``--cpu`` uses gloo and the test-only torch kernels (tests/cpu_kernels.py) so
+the distributed host logic (stage groups, all-reduce placement, hand-off
+routes, token return) is exercised without a GPU; otherwise NCCL + the C-ABI
+kernels, one GPU per rank. Exits non-zero on mismatch.
+"""
+
+import argparse
+import os
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from paper_2311_11514_b200.config import TINY, preset
+from paper_2311_11514_b200.engine import Engine
+from paper_2311_11514_b200.plan import simple_plan
+from paper_2311_11514_b200.weights import init_host_weights, synthetic_prompts
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--plan", default="2,1")
+    ap.add_argument("--layers", default="3,1")
+    ap.add_argument("--model", default="tiny")
+    ap.add_argument("--dtype", default="fp32")
+    ap.add_argument("--cpu", action="store_true")
+    ap.add_argument("--graphs", action="store_true")
+    ap.add_argument("--batch", type=int, default=2)
+    ap.add_argument("--s-in", type=int, default=64)
+    ap.add_argument("--s-out", type=int, default=16)
+    a = ap.parse_args()
+    tps = [int(x) for x in a.plan.split(",")]
+    layers = [int(x) for x in a.layers.split(",")]
+    cfg = TINY if a.model == "tiny" else preset(a.model)
+    rank = int(os.environ["RANK"])
+    if a.cpu:
+        dist.init_process_group("gloo")
+        import cpu_kernels
+        kernels, device = cpu_kernels, "cpu"
+    else:
+        local = int(os.environ.get("LOCAL_RANK", rank))
+        torch.cuda.set_device(local)
+        device = torch.device("cuda", local)
+        dist.init_process_group("nccl", device_id=device)
+        kernels = None
+    prompt = synthetic_prompts(cfg, a.batch, a.s_in, seed=1)
+    eng = Engine(simple_plan(tps, layers), cfg, dtype=a.dtype, batch=a.batch, max_prompt=a.s_in,
+                 max_out=a.s_out, comm="dist", device=device, kernels=kernels, use_graphs=a.graphs)
+    res = eng.generate(prompt, a.s_out)
+    res2 = eng.generate(prompt, a.s_out)
+    ok = True
+    if rank == 0:
+        from oracle.llama_oracle import Oracle, bf16_weights
+        w = init_host_weights(cfg, 0)
+        if a.dtype == "bf16":
+            w = bf16_weights(w)
+        ids, _ = Oracle(cfg, w, act_bf16=a.dtype == "bf16").generate(prompt, a.s_out)
+        same = np.array_equal(res.ids, ids) and np.array_equal(res2.ids, ids)
+        print(f"plan {tps} layers {layers}: ids match oracle: {same}; decode {res.decode_s * 1e3:.1f} ms")
+        if a.dtype == "fp32":
+            ok = same
+        else:  # bf16: first token must agree, later ones may flip on tiny margins
+            ok = np.array_equal(res.ids[:, 0], ids[:, 0])
+    flag = torch.tensor([0 if ok else 1], dtype=torch.int32, device="cpu" if a.cpu else device)
+    dist.all_reduce(flag)
+    dist.barrier()
+    dist.destroy_process_group()
+    sys.exit(int(flag.item() != 0))
+
+
+if __name__ == "__main__":
+    main()
