@@ -74,6 +74,14 @@ class DistComm:
             if key in self.groups or len(key) == 1:
                 continue
             self.groups[key] = self.dist.new_group(ranks=sorted(key))
+        # one 2-rank communicator per hand-off link (stage j -> j+1, last -> first),
+        # so point-to-point traffic never serialises behind other collectives
+        self.pairs = {}
+        for r in roles:
+            for dst in tuple(r.send_to) + tuple(r.ids_send_to):
+                key = (min(r.device, dst), max(r.device, dst))
+                if key not in self.pairs and key[0] != key[1]:
+                    self.pairs[key] = self.dist.new_group(ranks=list(key))
 
     def all_reduce_sum(self, tensors, group):
         for t in tensors:
@@ -84,10 +92,10 @@ class DistComm:
             self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.groups[group])
 
     def send(self, t, src, dst):
-        self.dist.send(t.contiguous(), dst)
+        self.dist.send(t.contiguous(), dst, group=self.pairs.get((min(src, dst), max(src, dst))))
 
     def recv(self, t, src, dst):
-        self.dist.recv(t, src)
+        self.dist.recv(t, src, group=self.pairs.get((min(src, dst), max(src, dst))))
 
     def broadcast_ids(self, hist, b, s_out, src, device):
         buf = hist.contiguous() if hist is not None and self.rank == src else \

@@ -6,9 +6,21 @@
 //
 // Paged layout: cache[block][kv_head][page][hd]; token position p of seq b
 // lives in block block_table[b * max_blocks + p / page] at slot p % page.
+#include <cstdlib>
+
 #include "hx_common.cuh"
 
 namespace hx {
+
+// tensor-core variants (hx_attention_mma.cu)
+int launch_prefill_mma(const void *q, const void *kc, const void *vc, const int32_t *bt, const int32_t *sl, void *o,
+                       int batch, int s, int hq, int hkv, int hd, int page, int maxb, cudaStream_t st);
+int launch_decode_mma(int G, int hd, dim3 grid, const void *q, const void *kc, const void *vc, const int32_t *bt,
+                      const int32_t *sl, void *o, int hkv, int page, int maxb, float *ws, int *cnt, cudaStream_t st);
+static int g_attn_mma = [] {
+  const char *e = getenv("HX_ATTN_MMA");
+  return e ? atoi(e) : 1;
+}();
 
 __device__ __forceinline__ size_t page_index(const int32_t *bt, int b, int pos, int max_blocks, int page,
                                              int hkv, int kvh, int hd) {
@@ -396,6 +408,9 @@ extern "C" int hx_attn_decode_paged(const void *q, const void *k_cache, const vo
   }
   dim3 grid(batch * hkv, splits);
   const float scale = 1.0f / sqrtf((float)hd);
+  if (dtype == HX_BF16 && G >= 2 && (hd == 64 || hd == 128) && g_attn_mma)  // GQA: tensor cores
+    return launch_decode_mma(G, hd, grid, q, k_cache, v_cache, block_table, seq_lens, o, hkv, page_size, max_blocks,
+                             ws, cnt, as_stream(stream));
   cudaStream_t st = as_stream(stream);
 #define HX_ARGS grid, q, k_cache, v_cache, block_table, seq_lens, o, hkv, page_size, max_blocks, scale, ws, cnt, st
   if (dtype == HX_BF16) {
@@ -438,6 +453,9 @@ extern "C" int hx_attn_prefill(const void *q, const void *k_cache, const void *v
   if (!q || !k_cache || !v_cache || !block_table || !seq_lens || !o || hq % hkv) return HX_ERR_ARG;
   cudaStream_t st = as_stream(stream);
 #define HX_PF(T, D) return launch_prefill<T, D>(q, k_cache, v_cache, block_table, seq_lens, o, batch, s, hq, hkv, page_size, max_blocks, st)
+  if (dtype == HX_BF16 && (hd == 64 || hd == 128) && g_attn_mma)
+    return launch_prefill_mma(q, k_cache, v_cache, block_table, seq_lens, o, batch, s, hq, hkv, hd, page_size,
+                              max_blocks, st);
   if (dtype == HX_BF16) {
     switch (hd) {
       case 32: HX_PF(__nv_bfloat16, 32);

@@ -1,0 +1,431 @@
+// Tensor-core attention for bf16 mode: warp-level
+// m16n8k16 MMAs with the online softmax kept in registers.
+//
+//   attn_prefill_mma_kernel: causal prefill, CTA = 64 queries x 1 head x 1
+//     sequence, 4 warps x 16 query rows; K/V 64-key blocks gathered from the
+//     paged cache with cp.async into a double-buffered smem ring.
+//   attn_decode_mma_kernel: GQA decode (group G >= 2), CTA = (seq, kv head,
+//     split); the G query heads of the group form one 16-row query tile (rows
+//     >= G are zero), so each K/V byte read from HBM feeds G heads on the
+//     tensor core; the 4 warps take 16-key slices of each 64-key block and are
+//     merged in smem, splits through the workspace (last-CTA ticket).
+// Both are HBM/L2-bound on K/V; fp32 mode and MHA decode use the CUDA-core
+// kernels in hx_attention.cu.
+#include "hx_common.cuh"
+
+namespace hx {
+
+constexpr int AM_BQ = 64, AM_BKV = 64, AM_THREADS = 128;
+
+template <int HD>
+struct AttnSmem {
+  static constexpr int LD = HD + 8;  // 16-byte pad: conflict-free ldmatrix rows
+  static constexpr int TILE = AM_BKV * LD;
+};
+
+// gather a 64-key block of K and V rows (positions p0 + k0 ..) into smem
+template <int HD>
+__device__ __forceinline__ void load_kv_block(__nv_bfloat16 *ks, __nv_bfloat16 *vs, const __nv_bfloat16 *kc,
+                                              const __nv_bfloat16 *vc, const int32_t *btb, int p0, int k0,
+                                              int klim, int page, int hkv, int kvh) {
+  constexpr int LD = AttnSmem<HD>::LD;
+  constexpr int CH = HD / 8;  // 16-byte chunks per row
+  for (int i = threadIdx.x; i < AM_BKV * CH; i += AM_THREADS) {
+    const int r = i / CH, c = (i % CH) * 8;
+    const int kj = k0 + r;
+    __nv_bfloat16 *kd = ks + r * LD + c, *vd = vs + r * LD + c;
+    if (kj < klim) {
+      const int pos = p0 + kj;
+      const size_t off = (((size_t)btb[pos / page] * hkv + kvh) * page + pos % page) * HD + c;
+      cp_async16(kd, kc + off);
+      cp_async16(vd, vc + off);
+    } else {
+      *reinterpret_cast<uint4 *>(kd) = make_uint4(0, 0, 0, 0);
+      *reinterpret_cast<uint4 *>(vd) = make_uint4(0, 0, 0, 0);
+    }
+  }
+}
+
+// S[16 x 8*NT] = Q[16 x HD] . K[keys 16*kr .. , HD]^T for NT n-tiles (NT even)
+template <int HD, int NT>
+__device__ __forceinline__ void qk_tiles(float (*s)[4], const uint32_t (*qf)[4], const __nv_bfloat16 *ks,
+                                         int key_base, int lane) {
+  constexpr int LD = AttnSmem<HD>::LD;
+#pragma unroll
+  for (int j = 0; j < NT; ++j)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) s[j][e] = 0.f;
+#pragma unroll
+  for (int jj = 0; jj < NT / 2; ++jj) {
+#pragma unroll
+    for (int c = 0; c < HD / 16; ++c) {
+      const int row = key_base + 16 * jj + (lane & 7) + 8 * (lane >> 4);
+      const int col = 16 * c + 8 * ((lane >> 3) & 1);
+      uint32_t b0, b1, b2, b3;
+      ldsm_x4(smem_u32(ks + row * LD + col), b0, b1, b2, b3);
+      mma_bf16_16816(s[2 * jj], qf[c], b0, b1);
+      mma_bf16_16816(s[2 * jj + 1], qf[c], b2, b3);
+    }
+  }
+}
+
+// O[16 x HD] += P[16 x 16*KC] . V[keys key_base .., HD]; P from the S tiles
+template <int HD, int KC>
+__device__ __forceinline__ void pv_tiles(float (*o)[4], const float (*p)[4], const __nv_bfloat16 *vs, int key_base,
+                                         int lane) {
+  constexpr int LD = AttnSmem<HD>::LD;
+#pragma unroll
+  for (int kk = 0; kk < KC; ++kk) {
+    uint32_t a[4];
+    a[0] = pack_bf16(p[2 * kk][0], p[2 * kk][1]);
+    a[1] = pack_bf16(p[2 * kk][2], p[2 * kk][3]);
+    a[2] = pack_bf16(p[2 * kk + 1][0], p[2 * kk + 1][1]);
+    a[3] = pack_bf16(p[2 * kk + 1][2], p[2 * kk + 1][3]);
+#pragma unroll
+    for (int n = 0; n < HD / 8; n += 2) {
+      const int row = key_base + 16 * kk + (lane & 7) + 8 * ((lane >> 3) & 1);
+      const int col = 8 * n + 8 * (lane >> 4);
+      uint32_t b0, b1, b2, b3;
+      ldsm_x4_t(smem_u32(vs + row * LD + col), b0, b1, b2, b3);
+      mma_bf16_16816(o[n], a, b0, b1);
+      mma_bf16_16816(o[n + 1], a, b2, b3);
+    }
+  }
+}
+
+// online softmax over NT n-tiles of S (rows g / g+8 of the warp tile);
+// s is replaced by p = exp2(s * sl2 - m) and l accumulates per-thread partials
+template <int NT, int HDT>
+__device__ __forceinline__ void online_softmax(float (*s)[4], float (*o)[4], float *m, float *l, float sl2) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    float mx = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < NT; ++j) mx = fmaxf(mx, fmaxf(s[j][2 * h], s[j][2 * h + 1]));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    const float mn = fmaxf(m[h], mx * sl2);
+    const float base = mn == -INFINITY ? 0.f : mn;
+    const float corr = exp2f(m[h] - base);
+    float rs = 0.f;
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      s[j][2 * h] = exp2f(s[j][2 * h] * sl2 - base);
+      s[j][2 * h + 1] = exp2f(s[j][2 * h + 1] * sl2 - base);
+      rs += s[j][2 * h] + s[j][2 * h + 1];
+    }
+    l[h] = l[h] * corr + rs;
+    m[h] = mn;
+#pragma unroll
+    for (int n = 0; n < HDT; ++n) {
+      o[n][2 * h] *= corr;
+      o[n][2 * h + 1] *= corr;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ prefill
+template <int HD>
+__global__ void __launch_bounds__(AM_THREADS)
+    attn_prefill_mma_kernel(const __nv_bfloat16 *q, const __nv_bfloat16 *kc, const __nv_bfloat16 *vc,
+                            const int32_t *bt, const int32_t *seq_lens, __nv_bfloat16 *o, int s_len, int hq,
+                            int hkv, int page, int max_blocks, float sl2) {
+  pdl_trigger();
+  pdl_wait();
+  constexpr int LD = AttnSmem<HD>::LD;
+  extern __shared__ __align__(128) uint8_t smraw[];
+  __nv_bfloat16 *qs = reinterpret_cast<__nv_bfloat16 *>(smraw);
+  __nv_bfloat16 *ks = qs + AM_BQ * LD;  // [2][BKV][LD]
+  __nv_bfloat16 *vs = ks + 2 * AttnSmem<HD>::TILE;
+  const int nqt = gridDim.x;
+  const int qt = nqt - 1 - blockIdx.x;  // heaviest (last) query tiles first
+  const int h = blockIdx.y, b = blockIdx.z;
+  const int kvh = h / (hq / hkv);
+  const int p0 = seq_lens[b];
+  const int q0 = qt * AM_BQ;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int32_t *btb = bt + (size_t)b * max_blocks;
+
+  constexpr int CH = HD / 8;
+  for (int i = threadIdx.x; i < AM_BQ * CH; i += AM_THREADS) {
+    const int r = i / CH, c = (i % CH) * 8;
+    __nv_bfloat16 *d = qs + r * LD + c;
+    if (q0 + r < s_len)
+      cp_async16(d, q + (((size_t)b * s_len + q0 + r) * hq + h) * HD + c);
+    else
+      *reinterpret_cast<uint4 *>(d) = make_uint4(0, 0, 0, 0);
+  }
+  const int q_hi = min(s_len, q0 + AM_BQ);
+  const int nblk = (q_hi + AM_BKV - 1) / AM_BKV;
+  load_kv_block<HD>(ks, vs, kc, vc, btb, p0, 0, s_len, page, hkv, kvh);
+  cp_async_commit();
+
+  uint32_t qf[HD / 16][4];
+  float oacc[HD / 8][4];
+#pragma unroll
+  for (int n = 0; n < HD / 8; ++n)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) oacc[n][e] = 0.f;
+  float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
+  const int qa = q0 + 16 * warp + g;  // this thread's two query rows: qa, qa + 8
+
+  for (int kb = 0; kb < nblk; ++kb) {
+    const int buf = kb & 1;
+    if (kb + 1 < nblk) {
+      load_kv_block<HD>(ks + (buf ^ 1) * AttnSmem<HD>::TILE, vs + (buf ^ 1) * AttnSmem<HD>::TILE, kc, vc, btb, p0,
+                        (kb + 1) * AM_BKV, s_len, page, hkv, kvh);
+    }
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    if (kb == 0) {
+#pragma unroll
+      for (int c = 0; c < HD / 16; ++c) {
+        const int row = 16 * warp + (lane & 7) + 8 * ((lane >> 3) & 1);
+        const int col = 16 * c + 8 * (lane >> 4);
+        ldsm_x4(smem_u32(qs + row * LD + col), qf[c][0], qf[c][1], qf[c][2], qf[c][3]);
+      }
+    }
+    const __nv_bfloat16 *kb_s = ks + buf * AttnSmem<HD>::TILE;
+    const __nv_bfloat16 *vb_s = vs + buf * AttnSmem<HD>::TILE;
+    const int k0 = kb * AM_BKV;
+    if (k0 <= q0 + 16 * warp + 15) {  // warp-uniform causal skip of fully masked blocks
+      float s[8][4];
+      qk_tiles<HD, 8>(s, qf, kb_s, 0, lane);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int kj = k0 + 8 * j + 2 * t4 + (e & 1);
+          const int qi = qa + 8 * (e >> 1);
+          if (kj > qi || kj >= s_len) s[j][e] = -INFINITY;
+        }
+      online_softmax<8, HD / 8>(s, oacc, m, l, sl2);
+      pv_tiles<HD, 4>(oacc, s, vb_s, 0, lane);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int hh = 0; hh < 2; ++hh) {
+    l[hh] += __shfl_xor_sync(0xffffffffu, l[hh], 1);
+    l[hh] += __shfl_xor_sync(0xffffffffu, l[hh], 2);
+  }
+#pragma unroll
+  for (int hh = 0; hh < 2; ++hh) {
+    const int qi = qa + 8 * hh;
+    if (qi >= s_len) continue;
+    const float inv = 1.f / l[hh];
+    __nv_bfloat16 *dst = o + (((size_t)b * s_len + qi) * hq + h) * HD;
+#pragma unroll
+    for (int n = 0; n < HD / 8; ++n)
+      *reinterpret_cast<uint32_t *>(dst + 8 * n + 2 * t4) = pack_bf16(oacc[n][2 * hh] * inv, oacc[n][2 * hh + 1] * inv);
+  }
+}
+
+// ------------------------------------------------------------------ decode (GQA)
+template <int HD, int G>
+__global__ void __launch_bounds__(AM_THREADS)
+    attn_decode_mma_kernel(const __nv_bfloat16 *q, const __nv_bfloat16 *kc, const __nv_bfloat16 *vc,
+                           const int32_t *bt, const int32_t *seq_lens, __nv_bfloat16 *o, int hkv, int page,
+                           int max_blocks, float sl2, float *ws, int *counters) {
+  pdl_trigger();
+  pdl_wait();
+  constexpr int LD = AttnSmem<HD>::LD;
+  extern __shared__ __align__(128) uint8_t smraw[];
+  __nv_bfloat16 *qs = reinterpret_cast<__nv_bfloat16 *>(smraw);  // [16][LD]
+  __nv_bfloat16 *ks = qs + 16 * LD;                                // [2][BKV][LD]
+  __nv_bfloat16 *vs = ks + 2 * AttnSmem<HD>::TILE;
+  float *red = reinterpret_cast<float *>(ks);  // [4 warps][16 rows][HD + 2], reuses K/V after the loop
+  const int b = blockIdx.x / hkv, kvh = blockIdx.x % hkv;
+  const int split = blockIdx.y, splits = gridDim.y;
+  const int hq = hkv * G;
+  const int ctx = seq_lens[b] + 1;
+  const int chunk = (ctx + splits - 1) / splits;
+  const int t0 = split * chunk, t1 = min(ctx, t0 + chunk);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int32_t *btb = bt + (size_t)b * max_blocks;
+
+  constexpr int CH = HD / 8;
+  for (int i = threadIdx.x; i < 16 * CH; i += AM_THREADS) {
+    const int r = i / CH, c = (i % CH) * 8;
+    __nv_bfloat16 *d = qs + r * LD + c;
+    if (r < G)
+      cp_async16(d, q + ((size_t)b * hq + kvh * G + r) * HD + c);
+    else
+      *reinterpret_cast<uint4 *>(d) = make_uint4(0, 0, 0, 0);
+  }
+  const int nblk = t1 > t0 ? (t1 - t0 + AM_BKV - 1) / AM_BKV : 0;
+  if (nblk > 0) load_kv_block<HD>(ks, vs, kc, vc, btb, 0, t0, t1, page, hkv, kvh);
+  cp_async_commit();
+  uint32_t qf[HD / 16][4];
+  float oacc[HD / 8][4];
+#pragma unroll
+  for (int n = 0; n < HD / 8; ++n)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) oacc[n][e] = 0.f;
+  float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
+  cp_async_wait<0>();
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < HD / 16; ++c) {
+    const int row = (lane & 7) + 8 * ((lane >> 3) & 1);
+    const int col = 16 * c + 8 * (lane >> 4);
+    ldsm_x4(smem_u32(qs + row * LD + col), qf[c][0], qf[c][1], qf[c][2], qf[c][3]);
+  }
+  for (int kb = 0; kb < nblk; ++kb) {
+    const int buf = kb & 1;
+    if (kb + 1 < nblk)
+      load_kv_block<HD>(ks + (buf ^ 1) * AttnSmem<HD>::TILE, vs + (buf ^ 1) * AttnSmem<HD>::TILE, kc, vc, btb, 0,
+                        t0 + (kb + 1) * AM_BKV, t1, page, hkv, kvh);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const int k0 = t0 + kb * AM_BKV + 16 * warp;  // this warp's 16 keys
+    if (k0 < t1) {
+      float s[2][4];
+      qk_tiles<HD, 2>(s, qf, ks + buf * AttnSmem<HD>::TILE, 16 * warp, lane);
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (k0 + 8 * j + 2 * t4 + (e & 1) >= t1) s[j][e] = -INFINITY;
+      online_softmax<2, HD / 8>(s, oacc, m, l, sl2);
+      pv_tiles<HD, 1>(oacc, s, vs + buf * AttnSmem<HD>::TILE, 16 * warp, lane);
+    }
+    __syncthreads();
+  }
+  // merge the 4 warps: per row (head) m, l and O
+#pragma unroll
+  for (int hh = 0; hh < 2; ++hh) {
+    l[hh] += __shfl_xor_sync(0xffffffffu, l[hh], 1);
+    l[hh] += __shfl_xor_sync(0xffffffffu, l[hh], 2);
+  }
+  float *wr = red + (size_t)warp * 16 * (HD + 2);
+#pragma unroll
+  for (int hh = 0; hh < 2; ++hh) {
+    const int r = g + 8 * hh;
+#pragma unroll
+    for (int n = 0; n < HD / 8; ++n) {
+      wr[r * (HD + 2) + 8 * n + 2 * t4] = oacc[n][2 * hh];
+      wr[r * (HD + 2) + 8 * n + 2 * t4 + 1] = oacc[n][2 * hh + 1];
+    }
+    if (t4 == 0) {
+      wr[r * (HD + 2) + HD] = m[hh];
+      wr[r * (HD + 2) + HD + 1] = l[hh];
+    }
+  }
+  __syncthreads();
+  const size_t pair = (size_t)b * hkv + kvh;
+  for (int w = threadIdx.x; w < G * HD; w += AM_THREADS) {
+    const int r = w / HD, d = w % HD;
+    float M = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) M = fmaxf(M, red[(i * 16 + r) * (HD + 2) + HD]);
+    float L = 0.f, A = 0.f;
+    if (M != -INFINITY) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float c = exp2f(red[(i * 16 + r) * (HD + 2) + HD] - M);
+        L += red[(i * 16 + r) * (HD + 2) + HD + 1] * c;
+        A += red[(i * 16 + r) * (HD + 2) + d] * c;
+      }
+    }
+    if (splits == 1) {
+      o[((size_t)b * hq + kvh * G + r) * HD + d] = __float2bfloat16_rn(A / L);
+    } else {
+      float *part = ws + ((pair * splits + split) * G + r) * (HD + 2);
+      part[d] = A;
+      if (d == 0) { part[HD] = M; part[HD + 1] = L; }
+    }
+  }
+  if (splits == 1) return;
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int tk = atomicAdd(&counters[pair], 1);
+    s_last = tk == splits - 1;
+    if (s_last) counters[pair] = 0;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int w = threadIdx.x; w < G * HD; w += AM_THREADS) {
+    const int r = w / HD, d = w % HD;
+    float M = -INFINITY;
+    for (int s2 = 0; s2 < splits; ++s2) M = fmaxf(M, __ldcg(ws + ((pair * splits + s2) * G + r) * (HD + 2) + HD));
+    float L = 0.f, A = 0.f;
+    for (int s2 = 0; s2 < splits; ++s2) {
+      const float *part = ws + ((pair * splits + s2) * G + r) * (HD + 2);
+      const float ms = __ldcg(part + HD);
+      if (ms == -INFINITY) continue;
+      const float c = exp2f(ms - M);
+      L += __ldcg(part + HD + 1) * c;
+      A += __ldcg(part + d) * c;
+    }
+    o[((size_t)b * hq + kvh * G + r) * HD + d] = __float2bfloat16_rn(A / L);
+  }
+}
+
+template <int HD>
+static size_t prefill_smem() {
+  return sizeof(__nv_bfloat16) * (AM_BQ * AttnSmem<HD>::LD + 4 * AttnSmem<HD>::TILE);
+}
+template <int HD>
+static size_t decode_smem() {
+  static_assert(sizeof(float) * 4 * 16 * (HD + 2) <= sizeof(__nv_bfloat16) * 4 * AttnSmem<HD>::TILE, "red alias");
+  return sizeof(__nv_bfloat16) * (16 * AttnSmem<HD>::LD + 4 * AttnSmem<HD>::TILE);
+}
+
+template <int HD>
+static int launch_prefill_mma_hd(const void *q, const void *kc, const void *vc, const int32_t *bt, const int32_t *sl,
+                                 void *o, int batch, int s, int hq, int hkv, int page, int maxb, cudaStream_t st) {
+  const size_t smem = prefill_smem<HD>();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_prefill_mma_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  const float sl2 = 1.4426950408889634f / sqrtf((float)HD);
+  dim3 grid((s + AM_BQ - 1) / AM_BQ, hq, batch);
+  return launch(attn_prefill_mma_kernel<HD>, grid, dim3(AM_THREADS), smem, st, (const __nv_bfloat16 *)q,
+                (const __nv_bfloat16 *)kc, (const __nv_bfloat16 *)vc, bt, sl, (__nv_bfloat16 *)o, s, hq, hkv, page,
+                maxb, sl2);
+}
+
+int launch_prefill_mma(const void *q, const void *kc, const void *vc, const int32_t *bt, const int32_t *sl, void *o,
+                       int batch, int s, int hq, int hkv, int hd, int page, int maxb, cudaStream_t st) {
+  if (hd == 128) return launch_prefill_mma_hd<128>(q, kc, vc, bt, sl, o, batch, s, hq, hkv, page, maxb, st);
+  if (hd == 64) return launch_prefill_mma_hd<64>(q, kc, vc, bt, sl, o, batch, s, hq, hkv, page, maxb, st);
+  return HX_ERR_UNSUPPORTED;
+}
+
+template <int HD, int G>
+static int launch_decode_mma_g(dim3 grid, const void *q, const void *kc, const void *vc, const int32_t *bt,
+                               const int32_t *sl, void *o, int hkv, int page, int maxb, float *ws, int *cnt,
+                               cudaStream_t st) {
+  const size_t smem = decode_smem<HD>();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_decode_mma_kernel<HD, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  const float sl2 = 1.4426950408889634f / sqrtf((float)HD);
+  return launch(attn_decode_mma_kernel<HD, G>, grid, dim3(AM_THREADS), smem, st, (const __nv_bfloat16 *)q,
+                (const __nv_bfloat16 *)kc, (const __nv_bfloat16 *)vc, bt, sl, (__nv_bfloat16 *)o, hkv, page, maxb,
+                sl2, ws, cnt);
+}
+
+int launch_decode_mma(int G, int hd, dim3 grid, const void *q, const void *kc, const void *vc, const int32_t *bt,
+                      const int32_t *sl, void *o, int hkv, int page, int maxb, float *ws, int *cnt, cudaStream_t st) {
+#define HX_DM(HDV, GV) \
+  if (hd == HDV && G == GV) return launch_decode_mma_g<HDV, GV>(grid, q, kc, vc, bt, sl, o, hkv, page, maxb, ws, cnt, st)
+  HX_DM(128, 2); HX_DM(128, 4); HX_DM(128, 8); HX_DM(128, 16);
+  HX_DM(64, 2); HX_DM(64, 4); HX_DM(64, 8); HX_DM(64, 16);
+#undef HX_DM
+  return HX_ERR_UNSUPPORTED;
+}
+
+}  // namespace hx

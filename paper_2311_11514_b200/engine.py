@@ -424,7 +424,8 @@ class Engine:
         for d in self.drivers:
             g = torch.cuda.CUDAGraph()
             n0 = self._launch_count()
-            with torch.cuda.graph(g):
+            # thread_local: the NCCL watchdog thread keeps querying events during capture
+            with torch.cuda.graph(g, capture_error_mode="thread_local"):
                 self._decode_compute(d, b)
             counts.append(self._launch_count() - n0)
             graphs.append(g)

@@ -212,7 +212,8 @@ def _paged_setup(dt, b, hq, hkv, hd, page, ctx_max, seed=0):
 
 @pytest.mark.parametrize("dt", [torch.float32, torch.bfloat16])
 @pytest.mark.parametrize("hq,hkv,hd,ctx", [(8, 8, 32, 70), (32, 32, 128, 600), (16, 2, 128, 1100),
-                                            (64, 8, 128, 300), (4, 4, 64, 1)])
+                                            (64, 8, 128, 300), (4, 4, 64, 1), (8, 4, 128, 333),
+                                            (16, 4, 64, 90), (16, 1, 128, 2), (32, 2, 128, 1279)])
 def test_rope_append_and_decode_attention(dt, hq, hkv, hd, ctx):
     b, page = 3, 16
     kc, vc, bt, g = _paged_setup(dt, b, hq, hkv, hd, page, ctx + 1)
@@ -248,7 +249,8 @@ def test_rope_append_and_decode_attention(dt, hq, hkv, hd, ctx):
 
 
 @pytest.mark.parametrize("dt", [torch.float32, torch.bfloat16])
-@pytest.mark.parametrize("hq,hkv,hd,s", [(8, 8, 32, 64), (4, 4, 128, 200), (8, 2, 128, 130), (2, 2, 64, 1)])
+@pytest.mark.parametrize("hq,hkv,hd,s", [(8, 8, 32, 64), (4, 4, 128, 200), (8, 2, 128, 130), (2, 2, 64, 1),
+                                          (4, 4, 64, 257), (2, 1, 128, 64), (1, 1, 128, 513)])
 def test_prefill_attention(dt, hq, hkv, hd, s):
     b, page = 2, 16
     kc, vc, bt, g = _paged_setup(dt, b, hq, hkv, hd, page, s)
