@@ -78,7 +78,10 @@ int hx_residual_add_rmsnorm(float *x, const float *delta, const float *gain,
  * y_dtype HX_F32 or HX_BF16; ldy = row pitch of Y in elements; flags:
  * HX_LINEAR_ACCUMULATE (Y += .., fp32 Y only), HX_LINEAR_PACKED (w is in the
  * hx_pack_weight tile layout). workspace >= hx_linear_workspace(...), its
- * first 16 KB (ticket counters) zeroed once before first use. */
+ * first 16 KB (ticket counters) zeroed once before first use.
+ * Under PDL the kernel streams its first weight tiles before waiting on the
+ * previous kernel: W must not be written by the kernel launched just before
+ * it on the stream (weights are static; hx_pack_weight never triggers early). */
 enum hx_linear_flags { HX_LINEAR_ACCUMULATE = 1, HX_LINEAR_PACKED = 2 };
 int hx_linear(const void *w, const void *x, void *y, int dtype, int y_dtype,
               int n_tok, int n_out, int k_dim, int ldy, int flags,

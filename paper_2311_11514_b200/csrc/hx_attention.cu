@@ -21,6 +21,11 @@ static int g_attn_mma = [] {
   const char *e = getenv("HX_ATTN_MMA");
   return e ? atoi(e) : 1;
 }();
+// smallest GQA group routed to the tensor-core decode kernel (1 = MHA too)
+static int g_attn_mma_min_group = [] {
+  const char *e = getenv("HX_ATTN_MMA_MIN_G");
+  return e ? atoi(e) : 2;
+}();
 
 __device__ __forceinline__ size_t page_index(const int32_t *bt, int b, int pos, int max_blocks, int page,
                                              int hkv, int kvh, int hd) {
@@ -350,6 +355,12 @@ static int launch_decode_g(int G, dim3 grid, const void *q, const void *kc, cons
     case 2: HX_DEC(2); break;
     case 4: HX_DEC(4); break;
     case 8: HX_DEC(8); break;
+    case 16:
+      if constexpr (sizeof(T) == 4) {  // bf16 G=16 always takes the tensor-core kernel
+        HX_DEC(16);
+      } else {
+        return HX_ERR_UNSUPPORTED;
+      }
     default: return HX_ERR_UNSUPPORTED;
   }
 #undef HX_DEC
@@ -408,7 +419,7 @@ extern "C" int hx_attn_decode_paged(const void *q, const void *k_cache, const vo
   }
   dim3 grid(batch * hkv, splits);
   const float scale = 1.0f / sqrtf((float)hd);
-  if (dtype == HX_BF16 && G >= 2 && (hd == 64 || hd == 128) && g_attn_mma)  // GQA: tensor cores
+  if (dtype == HX_BF16 && G >= g_attn_mma_min_group && (hd == 64 || hd == 128) && g_attn_mma)  // tensor cores
     return launch_decode_mma(G, hd, grid, q, k_cache, v_cache, block_table, seq_lens, o, hkv, page_size, max_blocks,
                              ws, cnt, as_stream(stream));
   cudaStream_t st = as_stream(stream);

@@ -422,8 +422,8 @@ int launch_decode_mma(int G, int hd, dim3 grid, const void *q, const void *kc, c
                       const int32_t *sl, void *o, int hkv, int page, int maxb, float *ws, int *cnt, cudaStream_t st) {
 #define HX_DM(HDV, GV) \
   if (hd == HDV && G == GV) return launch_decode_mma_g<HDV, GV>(grid, q, kc, vc, bt, sl, o, hkv, page, maxb, ws, cnt, st)
-  HX_DM(128, 2); HX_DM(128, 4); HX_DM(128, 8); HX_DM(128, 16);
-  HX_DM(64, 2); HX_DM(64, 4); HX_DM(64, 8); HX_DM(64, 16);
+  HX_DM(128, 1); HX_DM(128, 2); HX_DM(128, 4); HX_DM(128, 8); HX_DM(128, 16);
+  HX_DM(64, 1); HX_DM(64, 2); HX_DM(64, 4); HX_DM(64, 8); HX_DM(64, 16);
 #undef HX_DM
   return HX_ERR_UNSUPPORTED;
 }

@@ -436,7 +436,8 @@ __global__ void __launch_bounds__(192, 2)
 // dst[(t * KB + kb) * 128 * 64 + r * 64 + c] = src[(t * 128 + r) * K + kb * 64 + c] (0 if OOB)
 __global__ void pack_weight_kernel(const __nv_bfloat16 *__restrict__ src, __nv_bfloat16 *__restrict__ dst,
                                    int N, int K, int KB) {
-  pdl_trigger();
+  // no pdl_trigger(): a dependent GEMM prefetches weight tiles before its
+  // griddepcontrol.wait, so it must not start until the packed weights exist
   pdl_wait();
   const size_t tile = blockIdx.x;  // t * KB + kb
   const int t = (int)(tile / KB), kb = (int)(tile % KB);
