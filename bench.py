@@ -254,10 +254,33 @@ def gemm_roofline(eng, cfg, w, hbm, reps=5):
     torch.cuda.synchronize()
     t = s0.elapsed_time(s1) / 1e3 / reps
     achieved = nbytes / t / 1e9
-    return {"bound": "hbm", "kernel": "hx_linear (tcgen05 decode GEMM, split-K)", "achieved": round(achieved, 1),
+    # per projection shape: the same GEMM over every layer's weights, back to back
+    per_shape = {}
+    names = ["qkv", "o", "gate_up", "down"]
+    for i, name in enumerate(names):
+        sub = seq[i:4 * len(e.w["layers"]):4]
+        if not sub:
+            continue
+        gb = sum(wt.shape[0] * wt.shape[1] * 2 + b * wt.shape[1] * 2 + b * wt.shape[0] * y.element_size()
+                 for wt, xin, y in sub)
+        g2 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g2):
+            for wt, xin, y in sub:
+                ops.linear(wt, xin, y, b, e.lin_ws)
+        g2.replay()
+        torch.cuda.synchronize()
+        s0.record(st)
+        for _ in range(reps):
+            g2.replay()
+        s1.record(st)
+        torch.cuda.synchronize()
+        ts = s0.elapsed_time(s1) / 1e3 / reps
+        per_shape[name] = {"shape": list(sub[0][0].shape), "us_per_launch": round(ts / len(sub) * 1e6, 2),
+                           "GBps": round(gb / ts / 1e9, 1)}
+    return {"bound": "hbm", "kernel": "hx_linear (tcgen05 stream-K decode GEMM)", "achieved": round(achieved, 1),
             "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": None,
             "launches_per_step": len(seq), "avg_launch_us": round(t / len(seq) * 1e6, 2),
-            "bytes_per_step": nbytes, "gemm_ms_per_step": round(t * 1e3, 4)}
+            "bytes_per_step": nbytes, "gemm_ms_per_step": round(t * 1e3, 4), "per_shape": per_shape}
 
 
 def main():
@@ -371,10 +394,15 @@ def main():
             "clocks": clk,
             "cpu_baseline": cpu,
         }
-        print(json.dumps(line))
+        print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
-        dist.destroy_process_group()
+        torch.cuda.synchronize()
+        sys.stdout.flush()
+        sys.stderr.flush()
+        # NCCL communicators captured in CUDA graphs can hang destroy_process_group;
+        # the measurement is complete, so every rank exits directly.
+        os._exit(0)
     return 0
 
 

@@ -24,7 +24,7 @@ static int g_attn_mma = [] {
 // smallest GQA group routed to the tensor-core decode kernel (1 = MHA too)
 static int g_attn_mma_min_group = [] {
   const char *e = getenv("HX_ATTN_MMA_MIN_G");
-  return e ? atoi(e) : 2;
+  return e ? atoi(e) : 1;  // measured: MHA through the cp.async/mma kernel is also faster
 }();
 
 __device__ __forceinline__ size_t page_index(const int32_t *bt, int b, int pos, int max_blocks, int page,

@@ -38,9 +38,20 @@ extern int g_pdl;
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 
+// Every hx kernel runs with the maximum shared-memory carveout so the SM's
+// L1/smem split never has to be reconfigured (which drains the SM) between
+// consecutive kernels: a PDL-launched successor can become co-resident with
+// its predecessor's tail.
+void set_max_carveout(const void *fn);
+
 template <typename... KArgs, typename... Args>
 inline int launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                   Args &&...args) {
+  static bool configured = false;  // one flag per kernel instantiation
+  if (!configured) {
+    set_max_carveout(reinterpret_cast<const void *>(kern));
+    configured = true;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;

@@ -3,11 +3,19 @@
 // that follows each TP all-reduce, SwiGLU, greedy argmax (vocab-parallel) and
 // the per-step sequence-length advance. All are HBM/latency bound: one CTA per
 // token row, 16-byte vector accesses, fp32 math.
+#include <cstdlib>
+
 #include "hx_common.cuh"
 
 namespace hx {
 
 unsigned long long g_launches = 0;
+
+void set_max_carveout(const void *fn) {
+  const char *e = getenv("HX_MAX_CARVEOUT");
+  if (e && atoi(e) == 0) return;
+  cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+}
 int g_pdl = 1;
 
 constexpr int ROW_THREADS = 256;

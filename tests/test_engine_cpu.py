@@ -43,3 +43,16 @@ def test_kv_pages_are_interleaved_and_recycled():
         kv.assign(3, 100)
     kv.assign(2, 16)
     assert len(kv.owned) == 2 and len(kv.free) == kv.num_blocks - 2
+
+
+def test_measured_service_times_has_reference_table_shape():
+    """Same keys as the reference's service_times (simulate.py:135-142)."""
+    from paper_2311_11514_b200.plan import GlobalAssignment, StageAssignment
+    from paper_2311_11514_b200.serve import measured_service_times
+    ga = GlobalAssignment(((StageAssignment((0, 1), 3), StageAssignment((2,), 1)),
+                           (StageAssignment((3,), 4),)))
+    tasks = [TaskSpec(2, 8, 3), TaskSpec(2, 8, 3), TaskSpec(2, 16, 2)]
+    tab = measured_service_times(ga, TINY, tasks, comm="local", device="cpu", dtype="fp32",
+                                 weights="host", kernels=cpu_kernels)
+    assert set(tab) == {(r, t) for r in range(2) for t in set(tasks)}
+    assert all(v > 0 for v in tab.values())

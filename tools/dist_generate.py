@@ -75,9 +75,14 @@ def main():
             ok = np.array_equal(res.ids[:, 0], ids[:, 0])
     flag = torch.tensor([0 if ok else 1], dtype=torch.int32, device="cpu" if a.cpu else device)
     dist.all_reduce(flag)
-    dist.barrier()
-    dist.destroy_process_group()
-    sys.exit(int(flag.item() != 0))
+    code = int(flag.item() != 0)
+    if not a.cpu:
+        torch.cuda.synchronize()
+    sys.stdout.flush()
+    sys.stderr.flush()
+    # NCCL communicators referenced by captured CUDA graphs can hang in
+    # destroy_process_group at teardown; results are final, so leave directly.
+    os._exit(code)
 
 
 if __name__ == "__main__":
