@@ -1,0 +1,5 @@
+cd $GRAFT_REPO_ROOT
+timeout 600 python -m pytest tests/test_gpu_kernels.py -q -x 2>&1 | tail -1
+timeout 300 python tools/gemm_timeline.py --detail 2>&1 | grep -E "mean|total|slow:"
+timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/b10.json 2>/dev/null
+python -c "import json; d=json.load(open('gpurun_out/b10.json')); r=d['roofline']; print(d['value'], d['p50_decode_step_ms'], r['gemm_ms_per_step'], {k:v['GBps'] for k,v in r['per_shape'].items()})"

@@ -82,7 +82,15 @@ int hx_residual_add_rmsnorm(float *x, const float *delta, const float *gain,
  * Under PDL the kernel streams its first weight tiles before waiting on the
  * previous kernel: W must not be written by the kernel launched just before
  * it on the stream (weights are static; hx_pack_weight never triggers early). */
-enum hx_linear_flags { HX_LINEAR_ACCUMULATE = 1, HX_LINEAR_PACKED = 2 };
+enum hx_linear_flags { HX_LINEAR_ACCUMULATE = 1, HX_LINEAR_PACKED = 2, HX_LINEAR_DEFER_REDUCE = 4 };
+/* HX_LINEAR_DEFER_REDUCE (decode shapes, fp32 Y): tiles split across CTAs are
+ * left as fp32 partial slots in the workspace instead of being reduced by a
+ * ticketed last CTA; the next kernel on the stream must be
+ * hx_splitk_residual_rmsnorm with the same shape and workspace, which sums
+ * them in the same order (bitwise identical to the in-kernel reduction). */
+int hx_splitk_residual_rmsnorm(float *x, const float *y, int ldy, const void *workspace,
+                               int n_tok, int n_out, int k_dim, const float *gain,
+                               void *out, int out_dtype, float eps, hx_stream_t stream);
 int hx_linear(const void *w, const void *x, void *y, int dtype, int y_dtype,
               int n_tok, int n_out, int k_dim, int ldy, int flags,
               void *workspace, size_t workspace_bytes, hx_stream_t stream);
@@ -96,6 +104,13 @@ size_t hx_packed_weight_elems(int n_out, int k_dim);
 
 /* Programmatic dependent launch on/off for subsequent launches (default on). */
 void hx_set_pdl(int enabled);
+
+/* Profiling aid: subsequent decode-GEMM launches record, per CTA, 8 u64
+ * (globaltimer at start, after the dependency wait, at exit; SM id; first
+ * accumulator ready, first epilogue done, last accumulator ready; segments) into buf
+ * (device memory, `records` CTA slots). Returns the slots used since the
+ * previous call; buf = NULL disables. */
+size_t hx_debug_trace(void *buf, size_t records);
 
 /* out[t, j] = silu(gu[t, j]) * gu[t, inter + j], j < inter */
 int hx_swiglu(const void *gu, void *out, int dtype, int n_tok, int inter,

@@ -342,16 +342,14 @@ __global__ void __launch_bounds__(AM_THREADS)
   }
   if (splits == 1) return;
   __shared__ int s_last;
-  __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
-    const int tk = atomicAdd(&counters[pair], 1);
+    const int tk = ticket_acq_rel(&counters[pair]);
     s_last = tk == splits - 1;
     if (s_last) counters[pair] = 0;
   }
   __syncthreads();
   if (!s_last) return;
-  __threadfence();
   for (int w = threadIdx.x; w < G * HD; w += AM_THREADS) {
     const int r = w / HD, d = w % HD;
     float M = -INFINITY;

@@ -109,6 +109,21 @@ template <> struct Vec16<__nv_bfloat16> {
   }
 };
 
+// Split-K / split-KV ticket: acq_rel fence + atomic increment by one thread.
+// Writers: all threads store their partials, bar.sync, then one thread takes
+// the ticket (the fence releases the CTA's stores, cumulative through the
+// barrier). The thread drawing the last ticket has acquired every partial;
+// after the next bar.sync its CTA reads them with ld.cg. Much cheaper than a
+// sequentially consistent __threadfence() in every thread.
+__device__ __forceinline__ int ticket_acq_rel(int *counter) {
+  int old;
+  asm volatile("fence.acq_rel.gpu;\n\tatom.global.add.s32 %0, [%1], 1;\n\tfence.acq_rel.gpu;"
+               : "=r"(old)
+               : "l"(counter)
+               : "memory");
+  return old;
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

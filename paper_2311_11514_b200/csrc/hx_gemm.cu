@@ -201,16 +201,14 @@ __global__ void __launch_bounds__(128, 1)
       for (int j = 0; j < 16; j += 4)
         __stcg(reinterpret_cast<float4 *>(mine + c + j), make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
     }
-    __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
-      const int t = atomicAdd(&p.counters[tile], 1);
+      const int t = ticket_acq_rel(&p.counters[tile]);
       s_last = (t == splits - 1);
       if (s_last) p.counters[tile] = 0;  // re-arm for the next launch / graph replay
     }
     __syncthreads();
     if (s_last) {
-      __threadfence();
       const float *base = p.ws + ((size_t)tile * splits * BM + row) * BN;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 16) {
@@ -250,16 +248,30 @@ struct SKArgs {
   long ldm, ldn;
   int M, N;
   int c_bf16, accumulate, w_packed;
+  int defer;  // HX_LINEAR_DEFER_REDUCE: leave split tiles as partial slots (no ticket)
   int KB, units;
   float *ws;
   int *counters;
+  unsigned long long *trace;  // optional per-CTA timeline (hx_debug_trace): start, wait done, end, smid
 };
 
-__device__ __forceinline__ int sk_start(int c, int units, int G) { return (int)((long)c * units / G); }
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned s;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(s));
+  return s;
+}
+
+// c * units < 2^31 for every decode shape (units <= 4096 tiles x 172 K-blocks, G <= 296)
+__device__ __forceinline__ int sk_start(int c, int units, int G) { return (int)((unsigned)(c * units) / (unsigned)G); }
 
 // first CTA whose range contains unit u
 __device__ __forceinline__ int sk_owner(int u, int units, int G) {
-  int c = (int)((long)u * G / units);
+  int c = (int)((unsigned)(u * G) / (unsigned)units);
   while (c + 1 < G && sk_start(c + 1, units, G) <= u) ++c;
   while (c > 0 && sk_start(c, units, G) > u) --c;
   return c;
@@ -284,6 +296,7 @@ __global__ void __launch_bounds__(192, 2)
   __shared__ int s_last;
 
   pdl_trigger();
+  const unsigned long long t_start = p.trace ? globaltimer() : 0ull;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = gridDim.x, c = blockIdx.x;
   const int u0 = sk_start(c, p.units, G), u1 = sk_start(c + 1, p.units, G);
@@ -323,6 +336,7 @@ __global__ void __launch_bounds__(192, 2)
         load_w(i, u0 + i);
       }
       pdl_wait();
+      if (p.trace) p.trace[8 * c + 1] = globaltimer();
       for (int i = 0; i < pre; ++i) load_x(i, u0 + i);
       for (int i = pre; i < n; ++i) {
         const int s = i % STAGES;
@@ -371,6 +385,7 @@ __global__ void __launch_bounds__(192, 2)
       u = ue;
       const int buf = seg & 1;
       mbar_wait(&tfull[buf], (seg >> 1) & 1);
+      if (p.trace && etid == 0) p.trace[8 * c + (seg == 0 ? 4 : 6)] = globaltimer();
       tc_fence_after();
       const uint32_t tacc = tmem + ((uint32_t)(q * 32) << 16) + buf * BN;
       const int m = t * BM + row;
@@ -379,7 +394,9 @@ __global__ void __launch_bounds__(192, 2)
       ga.c_bf16 = p.c_bf16; ga.accumulate = p.accumulate;
       const bool whole = (kb_lo == 0 && kb_hi == p.KB);
       // partial tile: slot 2c (this CTA's first segment) or 2c+1 (its last)
-      float *mine = p.ws + ((size_t)(2 * c + (seg == 0 ? 0 : 1)) * BM + row) * BN;
+      // slot layout is token-major, ws[slot][token][row]: a warp's 32 rows are
+      // contiguous for every token, so stores here and loads in the reducers coalesce
+      float *mine = p.ws + (size_t)(2 * c + (seg == 0 ? 0 : 1)) * BM * BN + row;
 #pragma unroll 1
       for (int cc = 0; cc < BN; cc += 16) {
         float v[16];
@@ -388,38 +405,53 @@ __global__ void __launch_bounds__(192, 2)
           store_chunk(ga, m, cc, v);
         } else {
 #pragma unroll
-          for (int j = 0; j < 16; j += 4)
-            __stcg(reinterpret_cast<float4 *>(mine + cc + j), make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
+          for (int j = 0; j < 16; ++j) __stcg(mine + (size_t)(cc + j) * BM, v[j]);
         }
       }
       tc_fence_before();
       mbar_arrive(&tempty[buf]);
-      if (whole) continue;
-      __threadfence();
+      if (whole || p.defer) continue;  // deferred: the consuming kernel sums the slots
+      // release the partial (one thread, after the CTA-level barrier; acq_rel
+      // fences are cumulative through bar.sync) and take a ticket
       named_bar_sync(1, 128);
+      if (p.trace && etid == 0) p.trace[8 * c + 5] = globaltimer();
       const int c_first = sk_owner(t * p.KB, p.units, G);
       const int c_last = sk_owner((t + 1) * p.KB - 1, p.units, G);
       if (etid == 0) {
-        const int tk = atomicAdd(&p.counters[t], 1);
+        const int tk = ticket_acq_rel(&p.counters[t]);
         s_last = (tk == c_last - c_first);
         if (s_last) p.counters[t] = 0;
       }
       named_bar_sync(1, 128);
+      if (p.trace && etid == 0) p.trace[8 * c + 7] = globaltimer();
       if (s_last) {
-        __threadfence();
 #pragma unroll 1
         for (int ch = 0; ch < BN; ch += 16) {
           float acc[16];
 #pragma unroll
           for (int j = 0; j < 16; ++j) acc[j] = 0.f;
-          for (int cc = c_first; cc <= c_last; ++cc) {
-            // tile t is the first segment of cc unless cc started before the tile
-            const int sl = 2 * cc + (sk_start(cc, p.units, G) < t * p.KB ? 1 : 0);
-            const float *src = p.ws + ((size_t)sl * BM + row) * BN + ch;
+          // all contributors' partials are requested before any is summed (one L2
+          // round trip instead of one per contributor), then added in CTA order
+          constexpr int MAXC = 6;
+          for (int cb = c_first; cb <= c_last; cb += MAXC) {
+            float f[MAXC][16];
 #pragma unroll
-            for (int j = 0; j < 16; j += 4) {
-              const float4 f = __ldcg(reinterpret_cast<const float4 *>(src + j));
-              acc[j] += f.x; acc[j + 1] += f.y; acc[j + 2] += f.z; acc[j + 3] += f.w;
+            for (int i = 0; i < MAXC; ++i) {
+              const int cc = cb + i;
+              if (cc <= c_last) {
+                // tile t is the first segment of cc unless cc started before the tile
+                const int sl = 2 * cc + (sk_start(cc, p.units, G) < t * p.KB ? 1 : 0);
+                const float *src = p.ws + (size_t)sl * BM * BN + (size_t)ch * BM + row;
+#pragma unroll
+                for (int j = 0; j < 16; ++j) f[i][j] = __ldcg(src + (size_t)j * BM);
+              }
+            }
+#pragma unroll
+            for (int i = 0; i < MAXC; ++i) {
+              if (cb + i <= c_last) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) acc[j] += f[i][j];
+              }
             }
           }
           store_chunk(ga, m, ch, acc);
@@ -430,6 +462,102 @@ __global__ void __launch_bounds__(192, 2)
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tmem, TMEM_COLS);
+  if (p.trace && threadIdx.x == 0) {
+    p.trace[8 * c + 0] = t_start;
+    p.trace[8 * c + 2] = globaltimer();
+    p.trace[8 * c + 3] = smid();
+  }
+}
+
+// ------------------------------------------------------------------ deferred split-K consumer
+// x[t, :] += Y[t, :], Y = the preceding deferred stream-K GEMM's fp32 output:
+// whole tiles straight from y, split tiles summed from the partial slots in CTA
+// order (identical arithmetic to the in-kernel fixup); then the RMSNorm of x.
+// This moves the split-K reduction (two dependent L2 round trips under a
+// saturated memory system) off the GEMM's critical tail into a kernel that
+// reads its input anyway.
+struct SKView {
+  const float *ws;
+  int units, KB, G, BN;
+};
+
+__device__ __forceinline__ float4 sk_gather4(const SKView &v, const float *y, long ldy, int t, int n) {
+  const int tt = n / BM, r = n % BM;
+  const int c_first = sk_owner(tt * v.KB, v.units, v.G);
+  const int c_last = sk_owner((tt + 1) * v.KB - 1, v.units, v.G);
+  const bool whole = c_first == c_last && sk_start(c_first, v.units, v.G) <= tt * v.KB &&
+                     (c_first + 1 >= v.G ? v.units : sk_start(c_first + 1, v.units, v.G)) >= (tt + 1) * v.KB;
+  if (whole) return *reinterpret_cast<const float4 *>(y + (long)t * ldy + n);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  constexpr int MAXC = 8;  // all contributors' loads in flight together
+  for (int cb = c_first; cb <= c_last; cb += MAXC) {
+    float4 f[MAXC];
+#pragma unroll
+    for (int i = 0; i < MAXC; ++i) {
+      const int cc = cb + i;
+      if (cc <= c_last) {
+        const int sl = 2 * cc + (sk_start(cc, v.units, v.G) < tt * v.KB ? 1 : 0);
+        f[i] = __ldcg(reinterpret_cast<const float4 *>(v.ws + ((size_t)sl * v.BN + t) * BM + r));
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < MAXC; ++i) {
+      if (cb + i <= c_last) {
+        acc.x += f[i].x; acc.y += f[i].y; acc.z += f[i].z; acc.w += f[i].w;
+      }
+    }
+  }
+  return acc;
+}
+
+template <typename TO>
+__global__ void __launch_bounds__(1024)
+    sk_residual_rmsnorm_kernel(float *x, const float *y, long ldy, SKView v, const float *gain, TO *out, int hidden,
+                               float eps) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ float red[32];
+  const int t = blockIdx.x;
+  float *xr = x + (size_t)t * hidden;
+  constexpr int MAXV = 2;  // hidden <= 2 * 4 * 1024
+  float4 xv[MAXV], dv[MAXV];
+#pragma unroll
+  for (int i = 0; i < MAXV; ++i) {
+    const int n = (i * 1024 + threadIdx.x) * 4;
+    if (n < hidden) {
+      xv[i] = *reinterpret_cast<const float4 *>(xr + n);
+      dv[i] = sk_gather4(v, y, ldy, t, n);
+    }
+  }
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < MAXV; ++i) {
+    const int n = (i * 1024 + threadIdx.x) * 4;
+    if (n < hidden) {
+      xv[i].x += dv[i].x; xv[i].y += dv[i].y; xv[i].z += dv[i].z; xv[i].w += dv[i].w;
+      *reinterpret_cast<float4 *>(xr + n) = xv[i];
+      ss += xv[i].x * xv[i].x + xv[i].y * xv[i].y + xv[i].z * xv[i].z + xv[i].w * xv[i].w;
+    }
+  }
+  if (!out) return;
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  float tot = 0.f;
+  for (int i = 0; i < 32; ++i) tot += red[i];
+  const float inv = 1.0f / sqrtf(tot / (float)hidden + eps);
+  TO *o = out + (size_t)t * hidden;
+#pragma unroll
+  for (int i = 0; i < MAXV; ++i) {
+    const int n = (i * 1024 + threadIdx.x) * 4;
+    if (n < hidden) {
+      const float4 g = *reinterpret_cast<const float4 *>(gain + n);
+      o[n] = from_f32<TO>((xv[i].x * inv) * g.x);
+      o[n + 1] = from_f32<TO>((xv[i].y * inv) * g.y);
+      o[n + 2] = from_f32<TO>((xv[i].z * inv) * g.z);
+      o[n + 3] = from_f32<TO>((xv[i].w * inv) * g.w);
+    }
+  }
 }
 
 // ------------------------------------------------------------------ packing
@@ -610,6 +738,11 @@ static int sk_ctas_per_sm() {
   return v;
 }
 static int sk_grid(int units) { return std::min(units, sk_ctas_per_sm() * kNumSMs); }
+
+// debug timeline: 8 u64 per stream-K CTA (start, dependency-wait done, end, smid,
+// seg0 accumulator ready, seg0 epilogue done, last-seg accumulator ready, #segments)
+static unsigned long long *g_trace = nullptr;
+static size_t g_trace_cap = 0, g_trace_pos = 0;
 static int sk_grid_max(int units) { return std::min(units, 2 * kNumSMs); }
 
 extern "C" size_t hx_linear_workspace(int dtype, int n_tok, int n_out, int k_dim) {
@@ -632,6 +765,35 @@ static int launch_sk(const CUtensorMap &mw, const CUtensorMap &mx, const SKArgs 
     attr_done = true;
   }
   return launch(gemm_streamk_kernel<BN, STAGES>, dim3(sk_grid(p.units)), dim3(192), smem, st, mw, mx, p);
+}
+
+extern "C" int hx_splitk_residual_rmsnorm(float *x, const float *y, int ldy, const void *workspace, int n_tok,
+                                          int n_out, int k_dim, const float *gain, void *out, int out_dtype,
+                                          float eps, hx_stream_t stream) {
+  if (n_tok == 0) return 0;
+  if (!x || !y || !workspace || n_out % 4 || n_out > 8 * 4 * 256 || ldy % 4 || (out && !gain)) return HX_ERR_ARG;
+  Plan pl = plan_gemm(n_tok, n_out, k_dim);
+  if (!pl.decode) return HX_ERR_UNSUPPORTED;
+  SKView v;
+  v.ws = reinterpret_cast<const float *>(reinterpret_cast<const uint8_t *>(workspace) + kTicketBytes);
+  v.KB = (k_dim + BK - 1) / BK;
+  v.units = pl.tiles * v.KB;
+  v.G = sk_grid(v.units);
+  v.BN = pl.bn;
+  cudaStream_t st = as_stream(stream);
+  if (out_dtype == HX_BF16)
+    return launch(sk_residual_rmsnorm_kernel<__nv_bfloat16>, dim3(n_tok), dim3(1024), 0, st, x, y, (long)ldy, v, gain,
+                  (__nv_bfloat16 *)out, n_out, eps);
+  return launch(sk_residual_rmsnorm_kernel<float>, dim3(n_tok), dim3(1024), 0, st, x, y, (long)ldy, v, gain,
+                (float *)out, n_out, eps);
+}
+
+extern "C" size_t hx_debug_trace(void *buf, size_t records) {
+  const size_t used = g_trace_pos;
+  g_trace = reinterpret_cast<unsigned long long *>(buf);
+  g_trace_cap = buf ? records : 0;
+  g_trace_pos = 0;
+  return used;
 }
 
 extern "C" size_t hx_packed_weight_elems(int n_out, int k_dim) {
@@ -682,14 +844,33 @@ extern "C" int hx_linear(const void *w, const void *x, void *y, int dtype, int y
     SKArgs sk{};
     sk.c = y; sk.ldm = 1; sk.ldn = ldy; sk.M = n_out; sk.N = n_tok;
     sk.c_bf16 = p.c_bf16; sk.accumulate = accumulate; sk.w_packed = packed;
+    sk.defer = (flags & HX_LINEAR_DEFER_REDUCE) ? 1 : 0;
+    if (sk.defer && (p.c_bf16 || accumulate)) return HX_ERR_UNSUPPORTED;
     sk.KB = p.kb_total; sk.units = pl.tiles * p.kb_total;
     const size_t need = hx_linear_workspace(dtype, n_tok, n_out, k_dim);
     if (!workspace || workspace_bytes < need) return HX_ERR_WORKSPACE;
     if (pl.tiles > kMaxTickets) return HX_ERR_UNSUPPORTED;
     sk.counters = reinterpret_cast<int *>(workspace);
     sk.ws = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(workspace) + kTicketBytes);
+    const size_t g = (size_t)sk_grid(sk.units);
+    if (g_trace && g_trace_pos + g <= g_trace_cap) {
+      sk.trace = g_trace + 8 * g_trace_pos;
+      g_trace_pos += g;
+    }
     switch (pl.bn) {
-      case 16: return launch_sk<16, 6>(ma, mb, sk, st);
+      case 16: {
+        static const int stages = [] {
+          const char *e = getenv("HX_SK_STAGES");
+          return e ? atoi(e) : 6;
+        }();
+        switch (stages) {
+          case 4: return launch_sk<16, 4>(ma, mb, sk, st);
+          case 8: return launch_sk<16, 8>(ma, mb, sk, st);
+          case 10: return launch_sk<16, 10>(ma, mb, sk, st);
+          case 12: return launch_sk<16, 12>(ma, mb, sk, st);
+          default: return launch_sk<16, 6>(ma, mb, sk, st);
+        }
+      }
       case 32: return launch_sk<32, 5>(ma, mb, sk, st);
       default: return launch_sk<64, 4>(ma, mb, sk, st);
     }

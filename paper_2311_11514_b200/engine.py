@@ -153,7 +153,7 @@ class RankExecutor:
 
     def __init__(self, cfg: LlamaConfig, role: Role, dtype: torch.dtype, batch: int, max_prompt: int,
                  max_out: int, device, weights: dict, kernels=None, page_size: int = 64,
-                 pack_weights: bool = True):
+                 pack_weights: bool = True, defer_reduce: bool = True):
         self.cfg, self.role, self.dtype, self.device = cfg, role, dtype, torch.device(device)
         self.k = kernels or _ops
         self.w = weights
@@ -205,6 +205,9 @@ class RankExecutor:
         else:
             self.attn_ws_bytes = 0
         self.lin_ws = torch.zeros(max(ws, 256) // 4 + 64, dtype=torch.int32, device=dev)
+        self.defer = (tp == 1 and dtype == torch.bfloat16 and dev.type == "cuda" and self.k is _ops
+                      and defer_reduce)
+        self._defer_now = False
         self.attn_ws = torch.zeros(max(self.attn_ws_bytes, 256) // 4 + 64, dtype=torch.int32, device=dev)
 
     # ---- phases of layer li (local index) between the two all-reduces
@@ -222,19 +225,34 @@ class RankExecutor:
         else:
             k.attn_decode(self.q, kc, vc, self.kv.block_table, self.kv.seq_lens, self.attn, n_tok,
                           self.hq, self.hkv, self.hd, self.max_ctx, self.attn_ws)
-        k.linear(lw["wo"], self.attn, self.proj, n_tok, self.lin_ws)   # row-parallel partial
+        # TP=1 decode: the O/down GEMMs leave split tiles as partials and the
+        # residual+norm kernel that consumes them does the reduction
+        self._defer_now = self.defer and not prefill_len
+        self._linear(lw["wo"], self.attn, self.proj, n_tok)   # row-parallel partial
+
+    def _linear(self, w, x, y, n_tok):
+        if self._defer_now:
+            self.k.linear(w, x, y, n_tok, self.lin_ws, defer_reduce=True)
+        else:
+            self.k.linear(w, x, y, n_tok, self.lin_ws)
+
+    def _add_norm(self, k_dim, gain, out, n_tok):
+        if self._defer_now:
+            self.k.splitk_residual_rmsnorm(self.x, self.proj, self.lin_ws, n_tok, k_dim, gain, out,
+                                           self.cfg.rms_eps)
+        else:
+            self.k.residual_add_rmsnorm(self.x, self.proj, gain, out, n_tok, self.cfg.rms_eps)
 
     def mlp_block(self, li: int, n_tok: int):
-        k, cfg, lw = self.k, self.cfg, self.w["layers"][li]
-        k.residual_add_rmsnorm(self.x, self.proj, lw["ln_mlp"], self.h, n_tok, cfg.rms_eps)
+        k, lw = self.k, self.w["layers"][li]
+        self._add_norm(self.hq * self.hd, lw["ln_mlp"], self.h, n_tok)
         k.linear(lw["wgu"], self.h, self.gu, n_tok, self.lin_ws)
         k.swiglu(self.gu, self.a, n_tok)
-        k.linear(lw["wdown"], self.a, self.proj, n_tok, self.lin_ws)   # row-parallel partial
+        self._linear(lw["wdown"], self.a, self.proj, n_tok)   # row-parallel partial
 
     def post_block(self, li: int, n_tok: int):
         nxt = self.w["layers"][li + 1]["ln_attn"] if li + 1 < self.n_layers else None
-        self.k.residual_add_rmsnorm(self.x, self.proj, nxt, self.h if nxt is not None else None, n_tok,
-                                    self.cfg.rms_eps)
+        self._add_norm(self.inter, nxt, self.h if nxt is not None else None, n_tok)
 
     def head(self, prefill_len: int):
         """final norm on each sequence's last row + vocab-parallel lm_head + local argmax."""

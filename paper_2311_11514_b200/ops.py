@@ -35,6 +35,8 @@ _SIGS = {
     "hx_pack_weight": ([_P, _P, _I, _I, _P], _I),
     "hx_packed_weight_elems": ([_I, _I], _SZ),
     "hx_set_pdl": ([_I], None),
+    "hx_debug_trace": ([_P, _SZ], _SZ),
+    "hx_splitk_residual_rmsnorm": ([_P, _P, _I, _P, _I, _I, _I, _P, _P, _I, _F, _P], _I),
     "hx_swiglu": ([_P, _P, _I, _I, _I, _P], _I),
     "hx_rope_kv_append": ([_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _F, _P], _I),
     "hx_attn_decode_paged": ([_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _SZ, _P], _I),
@@ -148,11 +150,23 @@ def set_pdl(enabled: bool):
     load().hx_set_pdl(1 if enabled else 0)
 
 
-def linear(w, x, y, n_tok, workspace=None, accumulate=False):
+HX_LINEAR_DEFER_REDUCE = 4
+
+
+def splitk_residual_rmsnorm(x, y, workspace, n_tok, k_dim, gain, out, eps):
+    """Consumer of a deferred decode GEMM (linear(..., defer_reduce=True)) into y:
+    x += y (split tiles summed from the workspace slots); out = rmsnorm(x)*gain."""
+    n_out = x.shape[-1]
+    _check(load().hx_splitk_residual_rmsnorm(_p(x), _p(y), y.shape[-1], _p(workspace), n_tok, n_out, k_dim,
+                                             _p(gain), _p(out), dtype_code(out.dtype) if out is not None else HX_F32,
+                                             eps, _stream()), "hx_splitk_residual_rmsnorm")
+
+
+def linear(w, x, y, n_tok, workspace=None, accumulate=False, defer_reduce=False):
     """y[:n_tok, :n_out] (+)= x[:n_tok] @ w.T ; w [n_out, K] row-major tensor
-    or a PackedWeight."""
+    or a PackedWeight. defer_reduce: see splitk_residual_rmsnorm."""
     n_out, k = w.shape
-    flags = HX_LINEAR_ACCUMULATE if accumulate else 0
+    flags = (HX_LINEAR_ACCUMULATE if accumulate else 0) | (HX_LINEAR_DEFER_REDUCE if defer_reduce else 0)
     if isinstance(w, PackedWeight):
         flags |= HX_LINEAR_PACKED
         wp = w.data

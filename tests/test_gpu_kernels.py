@@ -97,6 +97,32 @@ def test_pdl_off_gives_identical_bits():
     assert torch.equal(y1, y2)
 
 
+@pytest.mark.parametrize("n_tok,H,k", [(8, 4096, 4096), (8, 4096, 11008), (32, 8192, 2048), (3, 2048, 5632),
+                                       (1, 256, 768)])
+def test_deferred_splitk_matches_in_kernel_reduction(n_tok, H, k):
+    """linear(defer_reduce) + splitk_residual_rmsnorm == linear + residual_add_rmsnorm, bitwise."""
+    w = ops.PackedWeight((torch.randn(H, k, device=DEV) * 0.02).bfloat16())
+    a = torch.randn(64, k, device=DEV).bfloat16()
+    gain = 1 + 0.1 * torch.randn(H, device=DEV)
+    x0 = torch.randn(64, H, device=DEV)
+    ws = torch.zeros(ops.linear_workspace(torch.bfloat16, n_tok, H, k) // 4 + 64, dtype=torch.int32, device=DEV)
+    y = torch.zeros(64, H, device=DEV)
+    x1, h1 = x0.clone(), torch.empty(64, H, device=DEV, dtype=torch.bfloat16)
+    ops.linear(w, a, y, n_tok, ws)
+    ops.residual_add_rmsnorm(x1, y, gain, h1, n_tok, 1e-5)
+    x2, h2 = x0.clone(), torch.empty(64, H, device=DEV, dtype=torch.bfloat16)
+    y2 = torch.zeros(64, H, device=DEV)
+    ops.linear(w, a, y2, n_tok, ws, defer_reduce=True)
+    ops.splitk_residual_rmsnorm(x2, y2, ws, n_tok, k, gain, h2, 1e-5)
+    x3 = x0.clone()
+    ops.linear(w, a, y2, n_tok, ws, defer_reduce=True)
+    ops.splitk_residual_rmsnorm(x3, y2, ws, n_tok, k, None, None, 1e-5)   # add only
+    torch.cuda.synchronize()
+    assert torch.equal(x1[:n_tok], x2[:n_tok]) and torch.equal(h1[:n_tok], h2[:n_tok])
+    assert torch.equal(x3[:n_tok], x1[:n_tok])
+    assert torch.equal(x2[n_tok:], x0[n_tok:])
+
+
 def test_linear_bf16_accumulate_and_pitch():
     w = (torch.randn(512, 256, device=DEV) * 0.05).bfloat16()
     x = torch.randn(8, 256, device=DEV).bfloat16()
