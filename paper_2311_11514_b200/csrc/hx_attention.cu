@@ -333,9 +333,12 @@ __global__ void __launch_bounds__(PF_THREADS)
 }
 
 static int decode_splits(int batch, int hkv, int max_ctx) {
+  // one wave: the tensor-core kernel keeps 2 CTAs (2 x 64 KB of K/V in flight)
+  // per SM, so splits = floor(2 * 148 / pairs) -- more would add a second,
+  // mostly idle wave; each split still streams several 64-key blocks
   const int pairs = batch * hkv;
-  const int target = 4 * 148;  // ~4 CTAs per SM keep enough KV bytes in flight
-  int s = (target + pairs - 1) / pairs;
+  const int target = 2 * 148;
+  int s = target / pairs;
   const int cap = (max_ctx + 63) / 64;
   s = s < cap ? s : cap;
   return s < 1 ? 1 : s;

@@ -16,6 +16,7 @@
 namespace hx {
 
 constexpr int AM_BQ = 64, AM_BKV = 64, AM_THREADS = 128;
+constexpr int DEC_NS = 3;  // decode K/V ring depth: 2 blocks (64 KB) in flight per CTA, 2 CTAs/SM
 
 template <int HD>
 struct AttnSmem {
@@ -234,8 +235,8 @@ __global__ void __launch_bounds__(AM_THREADS)
   constexpr int LD = AttnSmem<HD>::LD;
   extern __shared__ __align__(128) uint8_t smraw[];
   __nv_bfloat16 *qs = reinterpret_cast<__nv_bfloat16 *>(smraw);  // [16][LD]
-  __nv_bfloat16 *ks = qs + 16 * LD;                                // [2][BKV][LD]
-  __nv_bfloat16 *vs = ks + 2 * AttnSmem<HD>::TILE;
+  __nv_bfloat16 *ks = qs + 16 * LD;                                // [DEC_NS][BKV][LD]
+  __nv_bfloat16 *vs = ks + DEC_NS * AttnSmem<HD>::TILE;
   float *red = reinterpret_cast<float *>(ks);  // [4 warps][16 rows][HD + 2], reuses K/V after the loop
   const int b = blockIdx.x / hkv, kvh = blockIdx.x % hkv;
   const int split = blockIdx.y, splits = gridDim.y;
@@ -256,9 +257,15 @@ __global__ void __launch_bounds__(AM_THREADS)
     else
       *reinterpret_cast<uint4 *>(d) = make_uint4(0, 0, 0, 0);
   }
+  // DEC_NS-deep cp.async ring of 64-key K/V blocks (group 0 also carries Q)
   const int nblk = t1 > t0 ? (t1 - t0 + AM_BKV - 1) / AM_BKV : 0;
-  if (nblk > 0) load_kv_block<HD>(ks, vs, kc, vc, btb, 0, t0, t1, page, hkv, kvh);
-  cp_async_commit();
+#pragma unroll
+  for (int i = 0; i < DEC_NS - 1; ++i) {
+    if (i < nblk)
+      load_kv_block<HD>(ks + i * AttnSmem<HD>::TILE, vs + i * AttnSmem<HD>::TILE, kc, vc, btb, 0, t0 + i * AM_BKV, t1,
+                        page, hkv, kvh);
+    cp_async_commit();
+  }
   uint32_t qf[HD / 16][4];
   float oacc[HD / 8][4];
 #pragma unroll
@@ -266,22 +273,27 @@ __global__ void __launch_bounds__(AM_THREADS)
 #pragma unroll
     for (int e = 0; e < 4; ++e) oacc[n][e] = 0.f;
   float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
-  cp_async_wait<0>();
-  __syncthreads();
-#pragma unroll
-  for (int c = 0; c < HD / 16; ++c) {
-    const int row = (lane & 7) + 8 * ((lane >> 3) & 1);
-    const int col = 16 * c + 8 * (lane >> 4);
-    ldsm_x4(smem_u32(qs + row * LD + col), qf[c][0], qf[c][1], qf[c][2], qf[c][3]);
+  if (nblk == 0) {
+    cp_async_wait<0>();
+    __syncthreads();
   }
   for (int kb = 0; kb < nblk; ++kb) {
-    const int buf = kb & 1;
-    if (kb + 1 < nblk)
-      load_kv_block<HD>(ks + (buf ^ 1) * AttnSmem<HD>::TILE, vs + (buf ^ 1) * AttnSmem<HD>::TILE, kc, vc, btb, 0,
-                        t0 + (kb + 1) * AM_BKV, t1, page, hkv, kvh);
+    cp_async_wait<DEC_NS - 2>();  // block kb (and, at kb = 0, Q) has landed
+    __syncthreads();               // ... and every warp is done with block kb - 1's buffer
+    if (kb == 0) {
+#pragma unroll
+      for (int c = 0; c < HD / 16; ++c) {
+        const int row = (lane & 7) + 8 * ((lane >> 3) & 1);
+        const int col = 16 * c + 8 * (lane >> 4);
+        ldsm_x4(smem_u32(qs + row * LD + col), qf[c][0], qf[c][1], qf[c][2], qf[c][3]);
+      }
+    }
+    const int nb = kb + DEC_NS - 1;
+    if (nb < nblk)
+      load_kv_block<HD>(ks + (nb % DEC_NS) * AttnSmem<HD>::TILE, vs + (nb % DEC_NS) * AttnSmem<HD>::TILE, kc, vc,
+                        btb, 0, t0 + nb * AM_BKV, t1, page, hkv, kvh);
     cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();
+    const int buf = kb % DEC_NS;
     const int k0 = t0 + kb * AM_BKV + 16 * warp;  // this warp's 16 keys
     if (k0 < t1) {
       float s[2][4];
@@ -294,8 +306,9 @@ __global__ void __launch_bounds__(AM_THREADS)
       online_softmax<2, HD / 8>(s, oacc, m, l, sl2);
       pv_tiles<HD, 1>(oacc, s, vs + buf * AttnSmem<HD>::TILE, 16 * warp, lane);
     }
-    __syncthreads();
   }
+  cp_async_wait<0>();
+  __syncthreads();  // all warps done with K/V before `red` reuses that smem
   // merge the 4 warps: per row (head) m, l and O
 #pragma unroll
   for (int hh = 0; hh < 2; ++hh) {
@@ -373,8 +386,9 @@ static size_t prefill_smem() {
 }
 template <int HD>
 static size_t decode_smem() {
-  static_assert(sizeof(float) * 4 * 16 * (HD + 2) <= sizeof(__nv_bfloat16) * 4 * AttnSmem<HD>::TILE, "red alias");
-  return sizeof(__nv_bfloat16) * (16 * AttnSmem<HD>::LD + 4 * AttnSmem<HD>::TILE);
+  static_assert(sizeof(float) * 4 * 16 * (HD + 2) <= sizeof(__nv_bfloat16) * 2 * DEC_NS * AttnSmem<HD>::TILE,
+                "red alias");
+  return sizeof(__nv_bfloat16) * (16 * AttnSmem<HD>::LD + 2 * DEC_NS * AttnSmem<HD>::TILE);
 }
 
 template <int HD>
