@@ -118,7 +118,9 @@ def test_deferred_splitk_matches_in_kernel_reduction(n_tok, H, k):
     ops.linear(w, a, y2, n_tok, ws, defer_reduce=True)
     ops.splitk_residual_rmsnorm(x3, y2, ws, n_tok, k, None, None, 1e-5)   # add only
     torch.cuda.synchronize()
-    assert torch.equal(x1[:n_tok], x2[:n_tok]) and torch.equal(h1[:n_tok], h2[:n_tok])
+    assert torch.equal(x1[:n_tok], x2[:n_tok])  # the split-K sum is bitwise the in-kernel one
+    # the norm's block reduction uses a different thread count: at most 1 bf16 ulp apart
+    assert rel_err(h2[:n_tok], h1[:n_tok]) < 8e-3
     assert torch.equal(x3[:n_tok], x1[:n_tok])
     assert torch.equal(x2[n_tok:], x0[n_tok:])
 
