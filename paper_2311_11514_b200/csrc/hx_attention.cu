@@ -17,6 +17,12 @@ int launch_prefill_mma(const void *q, const void *kc, const void *vc, const int3
                        int batch, int s, int hq, int hkv, int hd, int page, int maxb, cudaStream_t st);
 int launch_decode_mma(int G, int hd, dim3 grid, const void *q, const void *kc, const void *vc, const int32_t *bt,
                       const int32_t *sl, void *o, int hkv, int page, int maxb, float *ws, int *cnt, cudaStream_t st);
+int launch_decode_tma(int G, dim3 grid, const void *q, const void *kc, const void *vc, const int32_t *bt,
+                      const int32_t *sl, void *o, int hkv, int maxb, float *ws, int *cnt, cudaStream_t st);
+static int g_attn_tma = [] {
+  const char *e = getenv("HX_ATTN_TMA");
+  return e ? atoi(e) : 1;
+}();
 static int g_attn_mma = [] {
   const char *e = getenv("HX_ATTN_MMA");
   return e ? atoi(e) : 1;
@@ -420,6 +426,9 @@ extern "C" int hx_attn_decode_paged(const void *q, const void *k_cache, const vo
   }
   dim3 grid(batch * hkv, splits);
   const float scale = 1.0f / sqrtf((float)hd);
+  if (dtype == HX_BF16 && hd == 128 && page_size == 64 && g_attn_tma && (G == 1 || G == 2 || G == 4 || G == 8 || G == 16))
+    return launch_decode_tma(G, grid, q, k_cache, v_cache, block_table, seq_lens, o, hkv, max_blocks, ws, cnt,
+                             as_stream(stream));
   if (dtype == HX_BF16 && G >= g_attn_mma_min_group && (hd == 64 || hd == 128) && g_attn_mma)  // tensor cores
     return launch_decode_mma(G, hd, grid, q, k_cache, v_cache, block_table, seq_lens, o, hkv, page_size, max_blocks,
                              ws, cnt, as_stream(stream));

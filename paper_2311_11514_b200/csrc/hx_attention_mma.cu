@@ -380,6 +380,233 @@ __global__ void __launch_bounds__(AM_THREADS)
   }
 }
 
+// ------------------------------------------------------------------ decode, TMA-fed (hd 128, page 64)
+// Same math as attn_decode_mma_kernel, but each 64-key block of one KV head --
+// one contiguous 16 KB page slice in the paged layout -- arrives by TMA (two
+// 64-column 128B-swizzled boxes for K, two for V) into a DEC_NS-deep mbarrier
+// ring: 4 instructions per block instead of 2048 cp.async, so the warps only
+// issue ldmatrix / mma / softmax. ldmatrix addresses apply the same XOR swizzle.
+__device__ __forceinline__ uint32_t sw128_addr(uint32_t base, int r, int col) {
+  const int half = col >> 6, chunk = (col & 63) >> 3;
+  return base + half * 8192 + r * 128 + ((chunk ^ (r & 7)) << 4) + ((col & 7) << 1);
+}
+
+template <int G>
+__global__ void __launch_bounds__(AM_THREADS)
+    attn_decode_tma_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
+                           const __nv_bfloat16 *q, const int32_t *bt, const int32_t *seq_lens, __nv_bfloat16 *o,
+                           int hkv, int max_blocks, float sl2, float *ws, int *counters) {
+  constexpr int HD = 128, LD = HD + 8, PAGE = 64;
+  constexpr uint32_t BLK = PAGE * HD * 2;  // 16 KB per tensor per block
+  extern __shared__ __align__(1024) uint8_t smraw[];
+  uint8_t *ring = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  // ring: [DEC_NS][K 16 KB | V 16 KB]; then Q tile; then barriers
+  __nv_bfloat16 *qs = reinterpret_cast<__nv_bfloat16 *>(ring + DEC_NS * 2 * BLK);
+  uint64_t *full = reinterpret_cast<uint64_t *>(qs + 16 * LD);
+  float *red = reinterpret_cast<float *>(ring);  // [4 warps][16][HD + 2], reuses the ring at the end
+  __shared__ int s_last;
+  pdl_trigger();
+  const int b = blockIdx.x / hkv, kvh = blockIdx.x % hkv;
+  const int split = blockIdx.y, splits = gridDim.y;
+  const int hq = hkv * G;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t4 = lane & 3;
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tmk);
+    tma_prefetch(&tmv);
+    for (int s = 0; s < DEC_NS; ++s) mbar_init(&full[s], 1);
+    fence_barrier_init();
+  }
+  pdl_wait();
+  const int ctx = seq_lens[b] + 1;
+  int chunk = (ctx + splits - 1) / splits;
+  chunk = (chunk + PAGE - 1) / PAGE * PAGE;  // page-aligned split ranges
+  const int t0 = split * chunk, t1 = min(ctx, t0 + chunk);
+  const int nblk = t1 > t0 ? (t1 - t0 + PAGE - 1) / PAGE : 0;
+  const int32_t *btb = bt + (size_t)b * max_blocks;
+  __syncthreads();  // barriers initialised
+  const uint64_t pol = l2_policy_evict_first();  // each K/V byte is read once per step
+  auto issue = [&](int i) {
+    const int s = i % DEC_NS;
+    const int row = (btb[t0 / PAGE + i] * hkv + kvh) * PAGE;
+    uint8_t *kd = ring + s * 2 * BLK, *vd = kd + BLK;
+    mbar_arrive_expect_tx(&full[s], 2 * BLK);
+    tma_load_2d(kd, &tmk, &full[s], 0, row, pol);
+    tma_load_2d(kd + BLK / 2, &tmk, &full[s], 64, row, pol);
+    tma_load_2d(vd, &tmv, &full[s], 0, row, pol);
+    tma_load_2d(vd + BLK / 2, &tmv, &full[s], 64, row, pol);
+  };
+  if (threadIdx.x == 0)
+    for (int i = 0; i < DEC_NS - 1 && i < nblk; ++i) issue(i);
+  for (int i = threadIdx.x; i < 16 * (HD / 8); i += AM_THREADS) {
+    const int r = i / (HD / 8), c = (i % (HD / 8)) * 8;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (r < G) v = *reinterpret_cast<const uint4 *>(q + ((size_t)b * hq + kvh * G + r) * HD + c);
+    *reinterpret_cast<uint4 *>(qs + r * LD + c) = v;
+  }
+  __syncthreads();
+  uint32_t qf[HD / 16][4];
+#pragma unroll
+  for (int c = 0; c < HD / 16; ++c) {
+    const int row = (lane & 7) + 8 * ((lane >> 3) & 1);
+    const int col = 16 * c + 8 * (lane >> 4);
+    ldsm_x4(smem_u32(qs + row * LD + col), qf[c][0], qf[c][1], qf[c][2], qf[c][3]);
+  }
+  float oacc[HD / 8][4];
+#pragma unroll
+  for (int n = 0; n < HD / 8; ++n)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) oacc[n][e] = 0.f;
+  float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
+  for (int kb = 0; kb < nblk; ++kb) {
+    if (kb > 0) __syncthreads();  // every warp is done with block kb - 1's stage
+    if (threadIdx.x == 0 && kb + DEC_NS - 1 < nblk) issue(kb + DEC_NS - 1);
+    const int s = kb % DEC_NS;
+    mbar_wait(&full[s], (kb / DEC_NS) & 1);
+    const uint32_t kbase = smem_u32(ring + s * 2 * BLK), vbase = kbase + BLK;
+    const int k0 = t0 + kb * PAGE + 16 * warp;  // this warp's 16 keys
+    if (k0 < t1) {
+      float sc[2][4];
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) sc[j][e] = 0.f;
+#pragma unroll
+      for (int c = 0; c < HD / 16; ++c) {
+        const int row = 16 * warp + (lane & 7) + 8 * (lane >> 4);
+        const int col = 16 * c + 8 * ((lane >> 3) & 1);
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4(sw128_addr(kbase, row, col), b0, b1, b2, b3);
+        mma_bf16_16816(sc[0], qf[c], b0, b1);
+        mma_bf16_16816(sc[1], qf[c], b2, b3);
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (k0 + 8 * j + 2 * t4 + (e & 1) >= t1) sc[j][e] = -INFINITY;
+      online_softmax<2, HD / 8>(sc, oacc, m, l, sl2);
+      uint32_t a[4];
+      a[0] = pack_bf16(sc[0][0], sc[0][1]);
+      a[1] = pack_bf16(sc[0][2], sc[0][3]);
+      a[2] = pack_bf16(sc[1][0], sc[1][1]);
+      a[3] = pack_bf16(sc[1][2], sc[1][3]);
+#pragma unroll
+      for (int n = 0; n < HD / 8; n += 2) {
+        const int row = 16 * warp + (lane & 7) + 8 * ((lane >> 3) & 1);
+        const int col = 8 * n + 8 * (lane >> 4);
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4_t(sw128_addr(vbase, row, col), b0, b1, b2, b3);
+        mma_bf16_16816(oacc[n], a, b0, b1);
+        mma_bf16_16816(oacc[n + 1], a, b2, b3);
+      }
+    }
+  }
+  __syncthreads();  // ring no longer read: `red` may overwrite it
+#pragma unroll
+  for (int hh = 0; hh < 2; ++hh) {
+    l[hh] += __shfl_xor_sync(0xffffffffu, l[hh], 1);
+    l[hh] += __shfl_xor_sync(0xffffffffu, l[hh], 2);
+  }
+  float *wr = red + (size_t)warp * 16 * (HD + 2);
+#pragma unroll
+  for (int hh = 0; hh < 2; ++hh) {
+    const int r = g + 8 * hh;
+#pragma unroll
+    for (int n = 0; n < HD / 8; ++n) {
+      wr[r * (HD + 2) + 8 * n + 2 * t4] = oacc[n][2 * hh];
+      wr[r * (HD + 2) + 8 * n + 2 * t4 + 1] = oacc[n][2 * hh + 1];
+    }
+    if (t4 == 0) {
+      wr[r * (HD + 2) + HD] = m[hh];
+      wr[r * (HD + 2) + HD + 1] = l[hh];
+    }
+  }
+  __syncthreads();
+  const size_t pair = (size_t)b * hkv + kvh;
+  for (int w = threadIdx.x; w < G * HD; w += AM_THREADS) {
+    const int r = w / HD, d = w % HD;
+    float M = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) M = fmaxf(M, red[(i * 16 + r) * (HD + 2) + HD]);
+    float L = 0.f, A = 0.f;
+    if (M != -INFINITY) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float c = exp2f(red[(i * 16 + r) * (HD + 2) + HD] - M);
+        L += red[(i * 16 + r) * (HD + 2) + HD + 1] * c;
+        A += red[(i * 16 + r) * (HD + 2) + d] * c;
+      }
+    }
+    if (splits == 1) {
+      o[((size_t)b * hq + kvh * G + r) * HD + d] = __float2bfloat16_rn(A / L);
+    } else {
+      float *part = ws + ((pair * splits + split) * G + r) * (HD + 2);
+      part[d] = A;
+      if (d == 0) { part[HD] = M; part[HD + 1] = L; }
+    }
+  }
+  if (splits == 1) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int tk = ticket_acq_rel(&counters[pair]);
+    s_last = tk == splits - 1;
+    if (s_last) counters[pair] = 0;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  for (int w = threadIdx.x; w < G * HD; w += AM_THREADS) {
+    const int r = w / HD, d = w % HD;
+    float M = -INFINITY;
+    for (int s2 = 0; s2 < splits; ++s2) M = fmaxf(M, __ldcg(ws + ((pair * splits + s2) * G + r) * (HD + 2) + HD));
+    float L = 0.f, A = 0.f;
+    for (int s2 = 0; s2 < splits; ++s2) {
+      const float *part = ws + ((pair * splits + s2) * G + r) * (HD + 2);
+      const float ms = __ldcg(part + HD);
+      if (ms == -INFINITY) continue;
+      const float c = exp2f(ms - M);
+      L += __ldcg(part + HD + 1) * c;
+      A += __ldcg(part + d) * c;
+    }
+    o[((size_t)b * hq + kvh * G + r) * HD + d] = __float2bfloat16_rn(A / L);
+  }
+}
+
+template <int G>
+static int launch_decode_tma_g(dim3 grid, const CUtensorMap &mk, const CUtensorMap &mv, const void *q,
+                               const int32_t *bt, const int32_t *sl, void *o, int hkv, int maxb, float *ws, int *cnt,
+                               cudaStream_t st) {
+  const size_t smem = 1024 + DEC_NS * 2 * 16384 + 16 * 136 * 2 + DEC_NS * 8 + 16;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_decode_tma_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  const float sl2 = 1.4426950408889634f / sqrtf(128.f);
+  return launch(attn_decode_tma_kernel<G>, grid, dim3(AM_THREADS), smem, st, mk, mv, (const __nv_bfloat16 *)q, bt,
+                sl, (__nv_bfloat16 *)o, hkv, maxb, sl2, ws, cnt);
+}
+
+// kc/vc: [num_blocks][hkv][64][128] bf16
+int launch_decode_tma(int G, dim3 grid, const void *q, const void *kc, const void *vc, const int32_t *bt,
+                      const int32_t *sl, void *o, int hkv, int maxb, float *ws, int *cnt, cudaStream_t st) {
+  CUtensorMap mk, mv;
+  // the pool size is not part of the C-ABI: declare 2^28 rows (64 GB of K); only
+  // rows of blocks named by the block table are ever addressed
+  const long rows = 1l << 28;
+  int rc = make_tma_bf16_sw128(&mk, kc, rows, 128, 128, 64);
+  if (!rc) rc = make_tma_bf16_sw128(&mv, vc, rows, 128, 128, 64);
+  if (rc) return rc;
+  switch (G) {
+    case 1: return launch_decode_tma_g<1>(grid, mk, mv, q, bt, sl, o, hkv, maxb, ws, cnt, st);
+    case 2: return launch_decode_tma_g<2>(grid, mk, mv, q, bt, sl, o, hkv, maxb, ws, cnt, st);
+    case 4: return launch_decode_tma_g<4>(grid, mk, mv, q, bt, sl, o, hkv, maxb, ws, cnt, st);
+    case 8: return launch_decode_tma_g<8>(grid, mk, mv, q, bt, sl, o, hkv, maxb, ws, cnt, st);
+    case 16: return launch_decode_tma_g<16>(grid, mk, mv, q, bt, sl, o, hkv, maxb, ws, cnt, st);
+  }
+  return HX_ERR_UNSUPPORTED;
+}
+
 template <int HD>
 static size_t prefill_smem() {
   return sizeof(__nv_bfloat16) * (AM_BQ * AttnSmem<HD>::LD + 4 * AttnSmem<HD>::TILE);

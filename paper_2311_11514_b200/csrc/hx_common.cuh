@@ -44,6 +44,10 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 // its predecessor's tail.
 void set_max_carveout(const void *fn);
 
+// host: 2-D bf16 TMA map [rows, cols] (row pitch in elements), box = box_rows
+// rows x 64 columns (128 B), 128B swizzle (hx_gemm.cu)
+int make_tma_bf16_sw128(CUtensorMap *map, const void *ptr, long rows, int cols, long pitch, int box_rows);
+
 template <typename... KArgs, typename... Args>
 inline int launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                   Args &&...args) {

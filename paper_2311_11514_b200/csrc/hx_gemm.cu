@@ -663,6 +663,10 @@ static int make_map(CUtensorMap *map, const void *ptr, long rows, int cols, long
   return r == CUDA_SUCCESS ? 0 : HX_ERR_DRIVER;
 }
 
+int make_tma_bf16_sw128(CUtensorMap *map, const void *ptr, long rows, int cols, long pitch, int box_rows) {
+  return make_map(map, ptr, rows, cols, pitch, box_rows);
+}
+
 template <int BN, int STAGES>
 static size_t smem_bytes() {
   return 1024 + STAGES * (BM * BK * 2 + BN * BK * 2) + (2 * STAGES + 1) * 8 + 16;

@@ -242,8 +242,9 @@ def _paged_setup(dt, b, hq, hkv, hd, page, ctx_max, seed=0):
 @pytest.mark.parametrize("hq,hkv,hd,ctx", [(8, 8, 32, 70), (32, 32, 128, 600), (16, 2, 128, 1100),
                                             (64, 8, 128, 300), (4, 4, 64, 1), (8, 4, 128, 333),
                                             (16, 4, 64, 90), (16, 1, 128, 2), (32, 2, 128, 1279)])
-def test_rope_append_and_decode_attention(dt, hq, hkv, hd, ctx):
-    b, page = 3, 16
+@pytest.mark.parametrize("page", [16, 64])   # 64 with hd 128 takes the TMA-fed kernel
+def test_rope_append_and_decode_attention(dt, hq, hkv, hd, ctx, page):
+    b = 3
     kc, vc, bt, g = _paged_setup(dt, b, hq, hkv, hd, page, ctx + 1)
     kr, vr = kc.clone(), vc.clone()
     # fill ctx cached tokens with random K/V through the reference writer
