@@ -112,6 +112,26 @@ void hx_set_pdl(int enabled);
  * previous call; buf = NULL disables. */
 size_t hx_debug_trace(void *buf, size_t records);
 
+/* ---- TP all-reduce over NVLink peer memory (decode), fused with residual+RMSNorm.
+ * Replaces NCCL all-reduce + hx_residual_add_rmsnorm after each row-parallel
+ * projection of a TP>1 stage (reference tp_comm_cost, costs.py:123-147).
+ * Buffers come from hx_ipc_alloc (zeroed cudaMalloc), are exported with
+ * hx_ipc_handle (64-byte cudaIpcMemHandle) and mapped on peers with hx_ipc_open.
+ * parts[r] = rank r's fp32 partial slot [n_tok][hidden] (peer-mapped; own local),
+ * flags[r] = rank r's int flag array [sites][max_tok][8]; site_state = this
+ * rank's int [sites][2] (zeroed). Every rank calls with the same site sequence;
+ * x[t] += sum_r parts[r][t] (rank order: bitwise identical on all ranks);
+ * out = rmsnorm(x) * gain (out may be NULL). Waits are bounded (trap, not hang). */
+int hx_ipc_alloc(void **ptr, size_t bytes);
+int hx_ipc_free(void *ptr);
+int hx_ipc_handle(void *ptr, void *handle64);
+int hx_ipc_open(const void *handle64, void **peer_ptr);
+int hx_ipc_close(void *peer_ptr);
+int hx_tp_allreduce_residual_rmsnorm(float *x, const float *const *parts, int *const *flags, int rank,
+                                     int tp, int site, int max_tok, int *site_state,
+                                     const float *gain, void *out, int out_dtype, int n_tok,
+                                     int hidden, float eps, hx_stream_t stream);
+
 /* out[t, j] = silu(gu[t, j]) * gu[t, inter + j], j < inter */
 int hx_swiglu(const void *gu, void *out, int dtype, int n_tok, int inter,
               hx_stream_t stream);

@@ -208,6 +208,8 @@ class RankExecutor:
         self.defer = (tp == 1 and dtype == torch.bfloat16 and dev.type == "cuda" and self.k is _ops
                       and defer_reduce)
         self._defer_now = False
+        self.par = None          # ops.PeerAllReduce when TP>1 ranks run in separate processes
+        self._peer_now = False
         self.attn_ws = torch.zeros(max(self.attn_ws_bytes, 256) // 4 + 64, dtype=torch.int32, device=dev)
 
     # ---- phases of layer li (local index) between the two all-reduces
@@ -228,7 +230,12 @@ class RankExecutor:
         # TP=1 decode: the O/down GEMMs leave split tiles as partials and the
         # residual+norm kernel that consumes them does the reduction
         self._defer_now = self.defer and not prefill_len
-        self._linear(lw["wo"], self.attn, self.proj, n_tok)   # row-parallel partial
+        # TP>1 decode: the partial goes straight into this rank's NVLink-visible slot
+        self._peer_now = self.par is not None and not prefill_len
+        self._linear(lw["wo"], self.attn, self._partial_out(2 * li), n_tok)   # row-parallel partial
+
+    def _partial_out(self, site):
+        return self.par.slot(site) if self._peer_now else self.proj
 
     def _linear(self, w, x, y, n_tok):
         if self._defer_now:
@@ -236,23 +243,25 @@ class RankExecutor:
         else:
             self.k.linear(w, x, y, n_tok, self.lin_ws)
 
-    def _add_norm(self, k_dim, gain, out, n_tok):
-        if self._defer_now:
+    def _add_norm(self, k_dim, gain, out, n_tok, site):
+        if self._peer_now:      # all-reduce over peer memory + residual + RMSNorm, one kernel
+            self.par.allreduce_residual_rmsnorm(self.x, site, gain, out, n_tok, self.cfg.rms_eps)
+        elif self._defer_now:   # TP=1: split-K reduction inside the residual+norm kernel
             self.k.splitk_residual_rmsnorm(self.x, self.proj, self.lin_ws, n_tok, k_dim, gain, out,
                                            self.cfg.rms_eps)
-        else:
+        else:                   # proj already all-reduced (NCCL) or TP=1 prefill
             self.k.residual_add_rmsnorm(self.x, self.proj, gain, out, n_tok, self.cfg.rms_eps)
 
     def mlp_block(self, li: int, n_tok: int):
         k, lw = self.k, self.w["layers"][li]
-        self._add_norm(self.hq * self.hd, lw["ln_mlp"], self.h, n_tok)
+        self._add_norm(self.hq * self.hd, lw["ln_mlp"], self.h, n_tok, 2 * li)
         k.linear(lw["wgu"], self.h, self.gu, n_tok, self.lin_ws)
         k.swiglu(self.gu, self.a, n_tok)
-        self._linear(lw["wdown"], self.a, self.proj, n_tok)   # row-parallel partial
+        self._linear(lw["wdown"], self.a, self._partial_out(2 * li + 1), n_tok)   # row-parallel partial
 
     def post_block(self, li: int, n_tok: int):
         nxt = self.w["layers"][li + 1]["ln_attn"] if li + 1 < self.n_layers else None
-        self._add_norm(self.inter, nxt, self.h if nxt is not None else None, n_tok)
+        self._add_norm(self.inter, nxt, self.h if nxt is not None else None, n_tok, 2 * li + 1)
 
     def head(self, prefill_len: int):
         """final norm on each sequence's last row + vocab-parallel lm_head + local argmax."""
@@ -280,7 +289,7 @@ class StageDriver:
         self.tp = self.role.tp
 
     def _ar(self, n_tok):
-        if self.tp > 1:
+        if self.tp > 1 and not self.execs[0]._peer_now:  # peer path reduces inside the next kernel
             self.comm.all_reduce_sum([e.proj[:n_tok] for e in self.execs], self.role.tp_group)
 
     def embed(self, n_tok: int, prefill: bool):
@@ -351,7 +360,8 @@ class Engine:
     def __init__(self, plan: GlobalAssignment, cfg: LlamaConfig, *, dtype: str = "bf16",
                  batch: int, max_prompt: int, max_out: int, pipeline: int = 0, comm: str = "local",
                  device=None, seed: int = 0, weights: str = "host", page_size: int = 64,
-                 use_graphs: bool = True, kernels=None, pack_weights: bool = True):
+                 use_graphs: bool = True, kernels=None, pack_weights: bool = True,
+                 peer_allreduce: bool = True):
         if dtype not in DTYPES:
             raise InputError(f"dtype must be one of {sorted(DTYPES)}")
         self.plan, self.cfg, self.dtype = plan, cfg, DTYPES[dtype]
@@ -378,6 +388,13 @@ class Engine:
                               load_rank_weights(cfg, r, self.dtype, self.device, seed, weights),
                               kernels=self.kernels, page_size=page_size,
                               pack_weights=pack_weights and kernels is None) for r in local]
+        import os
+        peer_allreduce = peer_allreduce and os.environ.get("HX_PEER_AR", "1") != "0"
+        if (peer_allreduce and self.comm.kind == "dist" and self.device.type == "cuda" and kernels is None):
+            for e in execs:
+                if e.role.tp > 1:  # fused NVLink all-reduce for the decode step
+                    e.par = _ops.PeerAllReduce(e.role.tp_rank, e.role.tp, batch, cfg.hidden_dim, 2 * e.n_layers,
+                                               self.comm.groups[e.role.tp_group], self.comm.dist)
         self.drivers = []
         for j in sorted({r.stage for r in local}):
             self.drivers.append(StageDriver([e for e in execs if e.role.stage == j], self.comm, j))

@@ -37,6 +37,13 @@ _SIGS = {
     "hx_set_pdl": ([_I], None),
     "hx_debug_trace": ([_P, _SZ], _SZ),
     "hx_splitk_residual_rmsnorm": ([_P, _P, _I, _P, _I, _I, _I, _P, _P, _I, _F, _P], _I),
+    "hx_ipc_alloc": ([ctypes.POINTER(ctypes.c_void_p), _SZ], _I),
+    "hx_ipc_free": ([_P], _I),
+    "hx_ipc_handle": ([_P, ctypes.c_char_p], _I),
+    "hx_ipc_open": ([ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)], _I),
+    "hx_ipc_close": ([_P], _I),
+    "hx_tp_allreduce_residual_rmsnorm": ([_P, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p),
+                                          _I, _I, _I, _I, _P, _P, _P, _I, _I, _I, _F, _P], _I),
     "hx_swiglu": ([_P, _P, _I, _I, _I, _P], _I),
     "hx_rope_kv_append": ([_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _F, _P], _I),
     "hx_attn_decode_paged": ([_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _SZ, _P], _I),
@@ -230,3 +237,64 @@ def argmax_finalize(keys, ids, history, step, n_tok, bump=True):
 
 def kv_bytes(dtype, layers, num_blocks, hkv_rank, page, hd) -> int:
     return int(load().hx_kv_bytes(dtype_code(dtype), layers, num_blocks, hkv_rank, page, hd))
+
+
+# ---------------------------------------------------------------- NVLink TP all-reduce
+class PeerAllReduce:
+    """Per-rank state of the fused NVLink all-reduce (hx_tp_allreduce_residual_rmsnorm):
+    two fp32 partial slots and a flag array in cudaIpc-exported memory, mapped on
+    every rank of the TP group (handles exchanged once over ``group``)."""
+
+    def __init__(self, rank: int, tp: int, max_tok: int, hidden: int, sites: int, group, dist):
+        lib = load()
+        self.rank, self.tp, self.max_tok, self.hidden, self.sites = rank, tp, max_tok, hidden, sites
+        slot_bytes = max_tok * hidden * 4
+        flag_bytes = sites * max_tok * 8 * 4
+        self._own = []
+        ptrs = {}
+        for name, nbytes in (("slot0", slot_bytes), ("slot1", slot_bytes), ("flags", flag_bytes)):
+            p = ctypes.c_void_p()
+            _check(lib.hx_ipc_alloc(ctypes.byref(p), nbytes), "hx_ipc_alloc")
+            self._own.append(p.value)
+            ptrs[name] = p.value
+        handles = {}
+        for name, p in ptrs.items():
+            h = ctypes.create_string_buffer(64)
+            _check(lib.hx_ipc_handle(p, h), "hx_ipc_handle")
+            handles[name] = h.raw
+        gathered = [None] * tp
+        dist.all_gather_object(gathered, handles, group=group)
+        self._opened = []
+        self.peer = {name: [0] * tp for name in ptrs}
+        for r in range(tp):
+            for name in ptrs:
+                if r == rank:
+                    self.peer[name][r] = ptrs[name]
+                else:
+                    q = ctypes.c_void_p()
+                    _check(lib.hx_ipc_open(gathered[r][name], ctypes.byref(q)), "hx_ipc_open")
+                    self.peer[name][r] = q.value
+                    self._opened.append(q.value)
+        self.site_state = torch.zeros(2 * sites, dtype=torch.int32, device="cuda")
+        self._arr = {name: (ctypes.c_void_p * tp)(*self.peer[name]) for name in ptrs}
+        dist.barrier(group=group)
+
+    def slot(self, site: int) -> torch.Tensor:
+        """This rank's partial slot for a call site, as a [max_tok, hidden] fp32 view."""
+        ptr = self.peer[f"slot{site % 2}"][self.rank]
+        return _tensor_at(ptr, (self.max_tok, self.hidden))
+
+    def allreduce_residual_rmsnorm(self, x, site, gain, out, n_tok, eps):
+        lib = load()
+        _check(lib.hx_tp_allreduce_residual_rmsnorm(
+            _p(x), self._arr[f"slot{site % 2}"], self._arr["flags"], self.rank, self.tp, site, self.max_tok,
+            _p(self.site_state), _p(gain), _p(out), dtype_code(out.dtype) if out is not None else HX_F32,
+            n_tok, self.hidden, eps, _stream()), "hx_tp_allreduce_residual_rmsnorm")
+
+
+def _tensor_at(ptr: int, shape) -> torch.Tensor:
+    """A torch view of raw device memory (owned elsewhere) via __cuda_array_interface__."""
+    class _Holder:
+        __cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<f4", "data": (ptr, False), "version": 3,
+                                    "strides": None}
+    return torch.as_tensor(_Holder(), device="cuda")

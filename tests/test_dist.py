@@ -54,6 +54,15 @@ def test_nccl_two_stage_fp32(plan, layers, graphs):
 
 
 @pytest.mark.gpu
+@pytest.mark.skipif(_gpus() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+def test_tp2_stage_nvlink_allreduce(dtype):
+    """Single TP=2 stage: the decode step's all-reduces run in the fused NVLink
+    peer-memory kernel (graphs on); ids must match the oracle."""
+    _run(2, ["--plan", "2", "--layers", "4", "--graphs", "--dtype", dtype])
+
+
+@pytest.mark.gpu
 @pytest.mark.skipif(_gpus() < 3, reason="needs >= 3 GPUs")
 def test_nccl_asymmetric_21_fp32_graphs():
     _run(3, ["--plan", "2,1", "--layers", "3,1", "--graphs"])
