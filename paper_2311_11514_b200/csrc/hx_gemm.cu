@@ -98,7 +98,18 @@ __global__ void __launch_bounds__(128, 1)
 
   pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  // grouped rasterisation: CTAs launched together cover a GM x (~148 / GM)
+  // block of tiles, so the activation rows and weight columns they share are
+  // read from HBM once and re-used from L2 (m-major order re-reads all of X for
+  // every weight tile once M outgrows one wave)
+  constexpr int GM = 16;
+  const int Mt = gridDim.x, Nt = gridDim.y;
+  const int pid = blockIdx.y * Mt + blockIdx.x;
+  const int first_m = (pid / (GM * Nt)) * GM;
+  const int gm = min(Mt - first_m, GM);
+  const int tm = first_m + (pid % (GM * Nt)) % gm;
+  const int tn = (pid % (GM * Nt)) / gm;
+  const int m0 = tm * BM, n0 = tn * BN;
   const int split = blockIdx.z, splits = gridDim.z;
   const int kb0 = split * p.kb_per_split;
   const int kb1 = min(p.kb_total, kb0 + p.kb_per_split);
@@ -126,14 +137,14 @@ __global__ void __launch_bounds__(128, 1)
     // weight operand: A (decode) or B (prefill); packed tiles are row blocks of a [*, 64] tensor
     auto load_w = [&](uint8_t *dst, int kb) {
       if (p.a_is_weight) {
-        if (p.w_packed) tma_load_2d(dst, &tm_a, &full[(dst - sa) / A_BYTES], 0, (blockIdx.x * p.kb_total + kb) * BM, pol_w);
+        if (p.w_packed) tma_load_2d(dst, &tm_a, &full[(dst - sa) / A_BYTES], 0, (tm * p.kb_total + kb) * BM, pol_w);
         else tma_load_2d(dst, &tm_a, &full[(dst - sa) / A_BYTES], kb * BK, m0, pol_w);
       } else {
         uint64_t *bar = &full[(dst - sb) / B_BYTES];
         if (p.w_packed) {
 #pragma unroll
           for (int h = 0; h < BN / BM; ++h)
-            tma_load_2d(dst + h * TILE_BYTES, &tm_b, bar, 0, ((blockIdx.y * (BN / BM) + h) * p.kb_total + kb) * BM, pol_w);
+            tma_load_2d(dst + h * TILE_BYTES, &tm_b, bar, 0, ((tn * (BN / BM) + h) * p.kb_total + kb) * BM, pol_w);
         } else {
           tma_load_2d(dst, &tm_b, bar, kb * BK, n0, pol_w);
         }
@@ -191,7 +202,7 @@ __global__ void __launch_bounds__(128, 1)
       store_chunk(p, m, n0 + c, v);
     }
   } else {
-    const int tile = blockIdx.y * gridDim.x + blockIdx.x;
+    const int tile = tn * Mt + tm;
     float *mine = p.ws + ((size_t)(tile * splits + split) * BM + row) * BN;
 #pragma unroll 1
     for (int c = 0; c < BN; c += 16) {
