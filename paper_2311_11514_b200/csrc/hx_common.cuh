@@ -44,6 +44,54 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 // its predecessor's tail.
 void set_max_carveout(const void *fn);
 
+// PDL launch with a thread-block cluster of `cluster_x` CTAs along x
+template <typename... KArgs, typename... Args>
+inline int launch_cluster(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                          int cluster_x, Args &&...args) {
+  static bool configured = false;
+  if (!configured) {
+    set_max_carveout(reinterpret_cast<const void *>(kern));
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = cluster_x;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+  ++g_launches;
+  if (e != cudaSuccess) return (int)e;
+  e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : (int)e;
+}
+
+// cluster helpers: rank in cluster, DSMEM read of another CTA's shared float, cluster barrier
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ float dsmem_ld_f32(const float *local_addr, unsigned cta) {
+  uint32_t remote;
+  const uint32_t local = static_cast<uint32_t>(__cvta_generic_to_shared(local_addr));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(cta));
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(remote) : "memory");
+  return v;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 // host: 2-D bf16 TMA map [rows, cols] (row pitch in elements), box = box_rows
 // rows x 64 columns (128 B), 128B swizzle (hx_gemm.cu)
 int make_tma_bf16_sw128(CUtensorMap *map, const void *ptr, long rows, int cols, long pitch, int box_rows);

@@ -521,21 +521,28 @@ __device__ __forceinline__ float4 sk_gather4(const SKView &v, const float *y, lo
   return acc;
 }
 
+constexpr int SK_CL = 4;
+
 template <typename TO>
-__global__ void __launch_bounds__(1024)
+__global__ void __launch_bounds__(256)
     sk_residual_rmsnorm_kernel(float *x, const float *y, long ldy, SKView v, const float *gain, TO *out, int hidden,
                                float eps) {
+  // one row = a cluster of SK_CL CTAs (each owns hidden / SK_CL features); the
+  // RMS sum of squares is combined across the cluster through DSMEM
   pdl_trigger();
   pdl_wait();
-  __shared__ float red[32];
-  const int t = blockIdx.x;
+  __shared__ float red[8];
+  __shared__ float part;
+  const unsigned cr = cluster_rank();
+  const int t = blockIdx.x / SK_CL;
+  const int per = hidden / SK_CL, base = (int)cr * per;
   float *xr = x + (size_t)t * hidden;
-  constexpr int MAXV = 2;  // hidden <= 2 * 4 * 1024
+  constexpr int MAXV = 2;  // hidden <= SK_CL * 2 * 4 * 256 = 8192
   float4 xv[MAXV], dv[MAXV];
 #pragma unroll
   for (int i = 0; i < MAXV; ++i) {
-    const int n = (i * 1024 + threadIdx.x) * 4;
-    if (n < hidden) {
+    const int n = base + (i * 256 + threadIdx.x) * 4;
+    if (n < base + per) {
       xv[i] = *reinterpret_cast<const float4 *>(xr + n);
       dv[i] = sk_gather4(v, y, ldy, t, n);
     }
@@ -543,25 +550,32 @@ __global__ void __launch_bounds__(1024)
   float ss = 0.f;
 #pragma unroll
   for (int i = 0; i < MAXV; ++i) {
-    const int n = (i * 1024 + threadIdx.x) * 4;
-    if (n < hidden) {
+    const int n = base + (i * 256 + threadIdx.x) * 4;
+    if (n < base + per) {
       xv[i].x += dv[i].x; xv[i].y += dv[i].y; xv[i].z += dv[i].z; xv[i].w += dv[i].w;
       *reinterpret_cast<float4 *>(xr + n) = xv[i];
       ss += xv[i].x * xv[i].x + xv[i].y * xv[i].y + xv[i].z * xv[i].z + xv[i].w * xv[i].w;
     }
   }
-  if (!out) return;
+  if (!out) return;  // uniform across the cluster
   ss = warp_sum(ss);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
   __syncthreads();
+  if (threadIdx.x == 0) {
+    float s = 0.f;
+    for (int i = 0; i < 8; ++i) s += red[i];
+    part = s;
+  }
+  cluster_sync_all();
   float tot = 0.f;
-  for (int i = 0; i < 32; ++i) tot += red[i];
+  for (int c = 0; c < SK_CL; ++c) tot += dsmem_ld_f32(&part, c);  // same order in every CTA
+  cluster_sync_all();  // peers have read `part` before this CTA may exit
   const float inv = 1.0f / sqrtf(tot / (float)hidden + eps);
   TO *o = out + (size_t)t * hidden;
 #pragma unroll
   for (int i = 0; i < MAXV; ++i) {
-    const int n = (i * 1024 + threadIdx.x) * 4;
-    if (n < hidden) {
+    const int n = base + (i * 256 + threadIdx.x) * 4;
+    if (n < base + per) {
       const float4 g = *reinterpret_cast<const float4 *>(gain + n);
       o[n] = from_f32<TO>((xv[i].x * inv) * g.x);
       o[n + 1] = from_f32<TO>((xv[i].y * inv) * g.y);
@@ -796,11 +810,12 @@ extern "C" int hx_splitk_residual_rmsnorm(float *x, const float *y, int ldy, con
   v.G = sk_grid(v.units);
   v.BN = pl.bn;
   cudaStream_t st = as_stream(stream);
+  if (n_out % (SK_CL * 4)) return HX_ERR_UNSUPPORTED;
   if (out_dtype == HX_BF16)
-    return launch(sk_residual_rmsnorm_kernel<__nv_bfloat16>, dim3(n_tok), dim3(1024), 0, st, x, y, (long)ldy, v, gain,
-                  (__nv_bfloat16 *)out, n_out, eps);
-  return launch(sk_residual_rmsnorm_kernel<float>, dim3(n_tok), dim3(1024), 0, st, x, y, (long)ldy, v, gain,
-                (float *)out, n_out, eps);
+    return launch_cluster(sk_residual_rmsnorm_kernel<__nv_bfloat16>, dim3(n_tok * SK_CL), dim3(256), 0, st, SK_CL, x,
+                          y, (long)ldy, v, gain, (__nv_bfloat16 *)out, n_out, eps);
+  return launch_cluster(sk_residual_rmsnorm_kernel<float>, dim3(n_tok * SK_CL), dim3(256), 0, st, SK_CL, x, y,
+                        (long)ldy, v, gain, (float *)out, n_out, eps);
 }
 
 extern "C" size_t hx_debug_trace(void *buf, size_t records) {
