@@ -1,0 +1,5 @@
+cd $GRAFT_REPO_ROOT
+timeout 900 python -m pytest tests -m gpu -q -rf > gpurun_out/pytest_full6.log 2>&1; echo rc=$?; tail -1 gpurun_out/pytest_full6.log; grep -E "^FAILED|Error" gpurun_out/pytest_full6.log | head -8
+timeout 600 python tools/ablate_step.py 2>&1 | grep -E "^none|all-but|norms|attn"
+timeout 300 python bench.py --steps 3 --warmup 3 > gpurun_out/b17.json 2>/dev/null
+tail -1 gpurun_out/b17.json | python -c "import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; print(d['value'], d['p50_decode_step_ms'], d['prefill_ms'], r['gemm_ms_per_step'], d['e2e']['value'], r['frac'])"

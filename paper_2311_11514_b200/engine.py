@@ -42,6 +42,15 @@ from .weights import _CODES, LAYER_TENSORS, init_tensor, shard_layer, tensor_sha
 DTYPES = {"bf16": torch.bfloat16, "fp32": torch.float32}
 
 
+def fused_epilogues() -> tuple[bool, bool]:
+    """(SwiGLU-in-gate/up-GEMM, RoPE+KV-append-in-decode-QKV-GEMM) for the bf16
+    tensor-core path; off by default (measured slower than the separate kernels at
+    7B batch 16), HX_FUSE_SWIGLU=1 / HX_FUSE_ROPE=1 enable them.
+    The bf16 oracle takes the same pair (rounding points differ between the two)."""
+    import os
+    return (os.environ.get("HX_FUSE_SWIGLU", "0") == "1", os.environ.get("HX_FUSE_ROPE", "0") == "1")
+
+
 # --------------------------------------------------------------------- weights
 def _device_tensor(cfg, seed, name, layer, device):
     """Synthetic weights generated on the device (fast path for large models):
@@ -157,9 +166,18 @@ class RankExecutor:
         self.cfg, self.role, self.dtype, self.device = cfg, role, dtype, torch.device(device)
         self.k = kernels or _ops
         self.w = weights
+        inter_r = cfg.intermediate // role.tp
+        # fused GEMM epilogues (bf16 tensor-core path): SwiGLU needs 64-row gate/up
+        # blocks, RoPE+KV-append needs 128-wide heads
+        tc = pack_weights and dtype == torch.bfloat16 and self.device.type == "cuda" and self.k is _ops
+        want_swiglu, want_rope = fused_epilogues()
+        self.fuse_swiglu = tc and want_swiglu and inter_r % 64 == 0
+        self.fuse_rope = tc and want_rope and cfg.head_dim == 128
         if pack_weights and dtype == torch.bfloat16 and self.device.type == "cuda":
             # tile-contiguous layout for the weight-streaming GEMM (hx_pack_weight)
             for lw in weights["layers"]:
+                if self.fuse_swiglu:
+                    lw["wgu"] = _ops.interleave_gate_up(lw["wgu"])
                 for name in ("wqkv", "wo", "wgu", "wdown"):
                     lw[name] = _ops.PackedWeight(lw[name])
             if "lm_head" in weights:
@@ -208,6 +226,7 @@ class RankExecutor:
         self.defer = (tp == 1 and dtype == torch.bfloat16 and dev.type == "cuda" and self.k is _ops
                       and defer_reduce)
         self._defer_now = False
+        self.rope_tab = _ops.rope_table(self.max_ctx, self.hd, cfg.rope_theta, dev) if self.fuse_rope else None
         self.par = None          # ops.PeerAllReduce when TP>1 ranks run in separate processes
         self._peer_now = False
         self.attn_ws = torch.zeros(max(self.attn_ws_bytes, 256) // 4 + 64, dtype=torch.int32, device=dev)
@@ -217,10 +236,14 @@ class RankExecutor:
         k, cfg, lw = self.k, self.cfg, self.w["layers"][li]
         if li == 0:  # input norm of the stage's first layer (x arrived raw)
             k.rmsnorm(self.x, lw["ln_attn"], self.h, n_tok, cfg.rms_eps)
-        k.linear(lw["wqkv"], self.h, self.qkv, n_tok, self.lin_ws)
         kc, vc = self.kv.k[li], self.kv.v[li]
-        k.rope_kv_append(self.qkv, self.q, kc, vc, self.kv.block_table, self.kv.seq_lens, n_tok,
-                         prefill_len, self.hq, self.hkv, self.hd, cfg.rope_theta)
+        if self.fuse_rope and not prefill_len:  # decode: QKV GEMM with RoPE + KV append in its epilogue
+            k.linear_rope_kv(lw["wqkv"], self.h, self.q, kc, vc, self.kv.block_table, self.kv.seq_lens, n_tok,
+                             prefill_len, self.hq, self.hkv, cfg.rope_theta, self.lin_ws, self.rope_tab)
+        else:
+            k.linear(lw["wqkv"], self.h, self.qkv, n_tok, self.lin_ws)
+            k.rope_kv_append(self.qkv, self.q, kc, vc, self.kv.block_table, self.kv.seq_lens, n_tok,
+                             prefill_len, self.hq, self.hkv, self.hd, cfg.rope_theta)
         if prefill_len:
             k.attn_prefill(self.q, kc, vc, self.kv.block_table, self.kv.seq_lens, self.attn,
                            n_tok // prefill_len, prefill_len, self.hq, self.hkv, self.hd)
@@ -255,8 +278,11 @@ class RankExecutor:
     def mlp_block(self, li: int, n_tok: int):
         k, lw = self.k, self.w["layers"][li]
         self._add_norm(self.hq * self.hd, lw["ln_mlp"], self.h, n_tok, 2 * li)
-        k.linear(lw["wgu"], self.h, self.gu, n_tok, self.lin_ws)
-        k.swiglu(self.gu, self.a, n_tok)
+        if self.fuse_swiglu:  # gate/up GEMM with SwiGLU in its epilogue (weights interleaved)
+            k.linear_swiglu(lw["wgu"], self.h, self.a, n_tok, self.lin_ws)
+        else:
+            k.linear(lw["wgu"], self.h, self.gu, n_tok, self.lin_ws)
+            k.swiglu(self.gu, self.a, n_tok)
         self._linear(lw["wdown"], self.a, self._partial_out(2 * li + 1), n_tok)   # row-parallel partial
 
     def post_block(self, li: int, n_tok: int):
