@@ -11,6 +11,7 @@
  *   hx_linear                 weight-scan + FLOP terms   costs.py:114-119
  *   hx_rope_kv_append,
  *   hx_attn_decode_paged,
+ *   hx_attn_decode_rope_append,
  *   hx_attn_prefill           attention / KV concat
  *   hx_residual_add_rmsnorm   "+ x" residual after each all-reduce
  *   hx_argmax_*               greedy token selection (not modelled by the reference)
@@ -179,6 +180,21 @@ int hx_attn_decode_paged(const void *q, const void *k_cache, const void *v_cache
                          void *workspace, size_t workspace_bytes,
                          hx_stream_t stream);
 size_t hx_attn_decode_workspace(int batch, int hq, int hkv, int hd, int max_ctx);
+
+/* hx_rope_kv_append + hx_attn_decode_paged of one decode step in one kernel:
+ * q comes un-rotated from the packed qkv rows ([batch][(hq + 2 hkv) * hd]);
+ * each CTA rotates its q heads, the CTA whose KV range holds position
+ * seq_lens[b] rotates that token's k and appends k, v to the page, and pages
+ * below the new token's page are prefetched before the kernel waits on the
+ * QKV producer. Results are bit-identical to the two separate calls. bf16,
+ * hd 128, page 64 only (else HX_ERR_UNSUPPORTED: use the separate calls);
+ * workspace as hx_attn_decode_workspace. */
+int hx_attn_decode_rope_append(const void *qkv, void *k_cache, void *v_cache,
+                               const int32_t *block_table, const int32_t *seq_lens,
+                               void *o, int dtype, int batch, int hq, int hkv, int hd,
+                               int page_size, int max_blocks, int max_ctx, float theta,
+                               void *workspace, size_t workspace_bytes,
+                               hx_stream_t stream);
 
 /* Causal prefill attention: q [batch*s, hq, hd] (roped), keys/values are the
  * s prompt tokens already appended to the paged cache (positions

@@ -18,7 +18,8 @@ int launch_prefill_mma(const void *q, const void *kc, const void *vc, const int3
 int launch_decode_mma(int G, int hd, dim3 grid, const void *q, const void *kc, const void *vc, const int32_t *bt,
                       const int32_t *sl, void *o, int hkv, int page, int maxb, float *ws, int *cnt, cudaStream_t st);
 int launch_decode_tma(int G, dim3 grid, const void *q, const void *kc, const void *vc, const int32_t *bt,
-                      const int32_t *sl, void *o, int hkv, int maxb, float *ws, int *cnt, cudaStream_t st);
+                      const int32_t *sl, void *o, int hkv, int maxb, float *ws, int *cnt, bool rope, float theta,
+                      cudaStream_t st);
 static int g_attn_tma = [] {
   const char *e = getenv("HX_ATTN_TMA");
   return e ? atoi(e) : 1;
@@ -66,8 +67,8 @@ __global__ void rope_append_kernel(const T *qkv, T *q_out, T *kc, T *vc, const i
   sincosf(ang, &sn, &cs);
   const float x1 = to_f32(src[i]);
   const float x2 = to_f32(src[i + half]);
-  const float y1 = x1 * cs - x2 * sn;  // x * cos + rotate_half(x) * sin
-  const float y2 = x2 * cs + x1 * sn;
+  const float2 y = rope_rot(x1, x2, cs, sn);  // x * cos + rotate_half(x) * sin
+  const float y1 = y.x, y2 = y.y;
   T *dst = h < hq ? q_out + ((size_t)t * hq + h) * hd
                   : kc + page_index(bt, b, pos, max_blocks, page, hkv, h - hq, hd);
   dst[i] = from_f32<T>(y1);
@@ -427,8 +428,8 @@ extern "C" int hx_attn_decode_paged(const void *q, const void *k_cache, const vo
   dim3 grid(batch * hkv, splits);
   const float scale = 1.0f / sqrtf((float)hd);
   if (dtype == HX_BF16 && hd == 128 && page_size == 64 && g_attn_tma && (G == 1 || G == 2 || G == 4 || G == 8 || G == 16))
-    return launch_decode_tma(G, grid, q, k_cache, v_cache, block_table, seq_lens, o, hkv, max_blocks, ws, cnt,
-                             as_stream(stream));
+    return launch_decode_tma(G, grid, q, k_cache, v_cache, block_table, seq_lens, o, hkv, max_blocks, ws, cnt, false,
+                             0.f, as_stream(stream));
   if (dtype == HX_BF16 && G >= g_attn_mma_min_group && (hd == 64 || hd == 128) && g_attn_mma)  // tensor cores
     return launch_decode_mma(G, hd, grid, q, k_cache, v_cache, block_table, seq_lens, o, hkv, page_size, max_blocks,
                              ws, cnt, as_stream(stream));
@@ -449,6 +450,30 @@ extern "C" int hx_attn_decode_paged(const void *q, const void *k_cache, const vo
   }
 #undef HX_ARGS
   return HX_ERR_UNSUPPORTED;
+}
+
+extern "C" int hx_attn_decode_rope_append(const void *qkv, void *k_cache, void *v_cache, const int32_t *block_table,
+                                          const int32_t *seq_lens, void *o, int dtype, int batch, int hq, int hkv,
+                                          int hd, int page_size, int max_blocks, int max_ctx, float theta,
+                                          void *workspace, size_t workspace_bytes, hx_stream_t stream) {
+  if (batch == 0) return 0;
+  if (!qkv || !k_cache || !v_cache || !block_table || !seq_lens || !o || hq % hkv) return HX_ERR_ARG;
+  const int G = hq / hkv;
+  if (dtype != HX_BF16 || hd != 128 || page_size != 64 || !g_attn_tma ||
+      !(G == 1 || G == 2 || G == 4 || G == 8 || G == 16))
+    return HX_ERR_UNSUPPORTED;
+  const int splits = decode_splits(batch, hkv, max_ctx);
+  float *ws = nullptr;
+  int *cnt = nullptr;
+  if (splits > 1) {
+    if (!workspace || workspace_bytes < hx_attn_decode_workspace(batch, hq, hkv, hd, max_ctx))
+      return HX_ERR_WORKSPACE;
+    if (batch * hkv > kMaxTickets) return HX_ERR_UNSUPPORTED;
+    cnt = reinterpret_cast<int *>(workspace);
+    ws = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(workspace) + kTicketBytes);
+  }
+  return launch_decode_tma(G, dim3(batch * hkv, splits), qkv, k_cache, v_cache, block_table, seq_lens, o, hkv,
+                           max_blocks, ws, cnt, true, theta, as_stream(stream));
 }
 
 template <typename T, int HD>

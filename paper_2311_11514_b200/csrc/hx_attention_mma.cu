@@ -391,11 +391,12 @@ __device__ __forceinline__ uint32_t sw128_addr(uint32_t base, int r, int col) {
   return base + half * 8192 + r * 128 + ((chunk ^ (r & 7)) << 4) + ((col & 7) << 1);
 }
 
-template <int G>
+template <int G, bool ROPE>
 __global__ void __launch_bounds__(AM_THREADS)
     attn_decode_tma_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
                            const __nv_bfloat16 *q, const int32_t *bt, const int32_t *seq_lens, __nv_bfloat16 *o,
-                           int hkv, int max_blocks, float sl2, float *ws, int *counters) {
+                           int hkv, int max_blocks, float sl2, float *ws, int *counters, __nv_bfloat16 *kc,
+                           __nv_bfloat16 *vc, float theta) {
   constexpr int HD = 128, LD = HD + 8, PAGE = 64;
   constexpr uint32_t BLK = PAGE * HD * 2;  // 16 KB per tensor per block
   extern __shared__ __align__(1024) uint8_t smraw[];
@@ -411,20 +412,19 @@ __global__ void __launch_bounds__(AM_THREADS)
   const int hq = hkv * G;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t4 = lane & 3;
-  if (threadIdx.x == 0) {
-    tma_prefetch(&tmk);
-    tma_prefetch(&tmv);
-    for (int s = 0; s < DEC_NS; ++s) mbar_init(&full[s], 1);
-    fence_barrier_init();
-  }
-  pdl_wait();
-  const int ctx = seq_lens[b] + 1;
+  // Before waiting on the producer of q / the new token's K,V: seq_lens and the
+  // block table are only written by hx_advance (which lets dependents launch only
+  // at its exit) and by the host, and every position < seq_lens[b] was appended in
+  // an earlier step -- so the pages wholly before the new token's page stream in
+  // while the QKV GEMM is still running.
+  const int pos = seq_lens[b];  // the new token's position
+  const int ctx = pos + 1;
   int chunk = (ctx + splits - 1) / splits;
   chunk = (chunk + PAGE - 1) / PAGE * PAGE;  // page-aligned split ranges
   const int t0 = split * chunk, t1 = min(ctx, t0 + chunk);
   const int nblk = t1 > t0 ? (t1 - t0 + PAGE - 1) / PAGE : 0;
   const int32_t *btb = bt + (size_t)b * max_blocks;
-  __syncthreads();  // barriers initialised
+  const int safe = min(nblk, max(0, pos / PAGE - t0 / PAGE));  // blocks not holding the new token
   const uint64_t pol = l2_policy_evict_first();  // each K/V byte is read once per step
   auto issue = [&](int i) {
     const int s = i % DEC_NS;
@@ -436,15 +436,59 @@ __global__ void __launch_bounds__(AM_THREADS)
     tma_load_2d(vd, &tmv, &full[s], 0, row, pol);
     tma_load_2d(vd + BLK / 2, &tmv, &full[s], 64, row, pol);
   };
-  if (threadIdx.x == 0)
-    for (int i = 0; i < DEC_NS - 1 && i < nblk; ++i) issue(i);
-  for (int i = threadIdx.x; i < 16 * (HD / 8); i += AM_THREADS) {
-    const int r = i / (HD / 8), c = (i % (HD / 8)) * 8;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (r < G) v = *reinterpret_cast<const uint4 *>(q + ((size_t)b * hq + kvh * G + r) * HD + c);
-    *reinterpret_cast<uint4 *>(qs + r * LD + c) = v;
+  const int pre = min(DEC_NS - 1, safe);
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tmk);
+    tma_prefetch(&tmv);
+    for (int s = 0; s < DEC_NS; ++s) mbar_init(&full[s], 1);
+    fence_barrier_init();
+    for (int i = 0; i < pre; ++i) issue(i);
+  }
+  pdl_wait();
+  if constexpr (ROPE) {
+    // q rows straight from the packed qkv row, rotated here (rotate-half pairs
+    // (i, i + 64), same fp32 arithmetic as rope_append_kernel); the CTA whose
+    // range holds the new token also rotates its k and appends k, v to the page
+    const int i = threadIdx.x & 63;
+    const __nv_bfloat16 *row = q + (size_t)b * (hq + 2 * hkv) * HD;
+    const float inv_freq = 1.0f / powf(theta, (float)(2 * i) / 128.0f);
+    float sn, cs;
+    sincosf((float)pos * inv_freq, &sn, &cs);
+    for (int r = threadIdx.x >> 6; r < 16; r += AM_THREADS / 64) {
+      float y1 = 0.f, y2 = 0.f;
+      if (r < G) {
+        const float x1 = to_f32(row[(kvh * G + r) * HD + i]), x2 = to_f32(row[(kvh * G + r) * HD + i + 64]);
+        const float2 y = rope_rot(x1, x2, cs, sn);
+        y1 = y.x;
+        y2 = y.y;
+      }
+      qs[r * LD + i] = __float2bfloat16_rn(y1);
+      qs[r * LD + i + 64] = __float2bfloat16_rn(y2);
+    }
+    if (t0 <= pos && pos < t1) {
+      const size_t slot = (((size_t)btb[pos / PAGE] * hkv + kvh) * PAGE + pos % PAGE) * HD;
+      if (threadIdx.x < 64) {
+        const float x1 = to_f32(row[(hq + kvh) * HD + i]), x2 = to_f32(row[(hq + kvh) * HD + i + 64]);
+        const float2 y = rope_rot(x1, x2, cs, sn);
+        kc[slot + i] = __float2bfloat16_rn(y.x);
+        kc[slot + i + 64] = __float2bfloat16_rn(y.y);
+      } else {
+        vc[slot + i] = row[(hq + hkv + kvh) * HD + i];
+        vc[slot + i + 64] = row[(hq + hkv + kvh) * HD + i + 64];
+      }
+      fence_proxy_async_global();  // the page is about to be read back by TMA
+    }
+  } else {
+    for (int i = threadIdx.x; i < 16 * (HD / 8); i += AM_THREADS) {
+      const int r = i / (HD / 8), c = (i % (HD / 8)) * 8;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (r < G) v = *reinterpret_cast<const uint4 *>(q + ((size_t)b * hq + kvh * G + r) * HD + c);
+      *reinterpret_cast<uint4 *>(qs + r * LD + c) = v;
+    }
   }
   __syncthreads();
+  if (threadIdx.x == 0)
+    for (int i = pre; i < DEC_NS - 1 && i < nblk; ++i) issue(i);
   uint32_t qf[HD / 16][4];
 #pragma unroll
   for (int c = 0; c < HD / 16; ++c) {
@@ -572,24 +616,26 @@ __global__ void __launch_bounds__(AM_THREADS)
   }
 }
 
-template <int G>
+template <int G, bool ROPE>
 static int launch_decode_tma_g(dim3 grid, const CUtensorMap &mk, const CUtensorMap &mv, const void *q,
                                const int32_t *bt, const int32_t *sl, void *o, int hkv, int maxb, float *ws, int *cnt,
-                               cudaStream_t st) {
+                               void *kc, void *vc, float theta, cudaStream_t st) {
   const size_t smem = 1024 + DEC_NS * 2 * 16384 + 16 * 136 * 2 + DEC_NS * 8 + 16;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(attn_decode_tma_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(attn_decode_tma_kernel<G, ROPE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
   const float sl2 = 1.4426950408889634f / sqrtf(128.f);
-  return launch(attn_decode_tma_kernel<G>, grid, dim3(AM_THREADS), smem, st, mk, mv, (const __nv_bfloat16 *)q, bt,
-                sl, (__nv_bfloat16 *)o, hkv, maxb, sl2, ws, cnt);
+  return launch(attn_decode_tma_kernel<G, ROPE>, grid, dim3(AM_THREADS), smem, st, mk, mv, (const __nv_bfloat16 *)q,
+                bt, sl, (__nv_bfloat16 *)o, hkv, maxb, sl2, ws, cnt, (__nv_bfloat16 *)kc, (__nv_bfloat16 *)vc, theta);
 }
 
-// kc/vc: [num_blocks][hkv][64][128] bf16
+// kc/vc: [num_blocks][hkv][64][128] bf16. rope: q is the packed qkv row and the
+// new token's k (rotated) and v are appended by the kernel itself.
 int launch_decode_tma(int G, dim3 grid, const void *q, const void *kc, const void *vc, const int32_t *bt,
-                      const int32_t *sl, void *o, int hkv, int maxb, float *ws, int *cnt, cudaStream_t st) {
+                      const int32_t *sl, void *o, int hkv, int maxb, float *ws, int *cnt, bool rope, float theta,
+                      cudaStream_t st) {
   CUtensorMap mk, mv;
   // the pool size is not part of the C-ABI: declare 2^28 rows (64 GB of K); only
   // rows of blocks named by the block table are ever addressed
@@ -597,13 +643,18 @@ int launch_decode_tma(int G, dim3 grid, const void *q, const void *kc, const voi
   int rc = make_tma_bf16_sw128(&mk, kc, rows, 128, 128, 64);
   if (!rc) rc = make_tma_bf16_sw128(&mv, vc, rows, 128, 128, 64);
   if (rc) return rc;
+  void *k = const_cast<void *>(kc), *v = const_cast<void *>(vc);
+#define HX_TMA_G(GG)                                                                                             \
+  return rope ? launch_decode_tma_g<GG, true>(grid, mk, mv, q, bt, sl, o, hkv, maxb, ws, cnt, k, v, theta, st) \
+              : launch_decode_tma_g<GG, false>(grid, mk, mv, q, bt, sl, o, hkv, maxb, ws, cnt, k, v, theta, st)
   switch (G) {
-    case 1: return launch_decode_tma_g<1>(grid, mk, mv, q, bt, sl, o, hkv, maxb, ws, cnt, st);
-    case 2: return launch_decode_tma_g<2>(grid, mk, mv, q, bt, sl, o, hkv, maxb, ws, cnt, st);
-    case 4: return launch_decode_tma_g<4>(grid, mk, mv, q, bt, sl, o, hkv, maxb, ws, cnt, st);
-    case 8: return launch_decode_tma_g<8>(grid, mk, mv, q, bt, sl, o, hkv, maxb, ws, cnt, st);
-    case 16: return launch_decode_tma_g<16>(grid, mk, mv, q, bt, sl, o, hkv, maxb, ws, cnt, st);
+    case 1: HX_TMA_G(1);
+    case 2: HX_TMA_G(2);
+    case 4: HX_TMA_G(4);
+    case 8: HX_TMA_G(8);
+    case 16: HX_TMA_G(16);
   }
+#undef HX_TMA_G
   return HX_ERR_UNSUPPORTED;
 }
 

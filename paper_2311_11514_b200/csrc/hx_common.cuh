@@ -32,7 +32,9 @@ inline cudaStream_t as_stream(hx_stream_t s) { return reinterpret_cast<cudaStrea
 // entry and waits (griddepcontrol.wait) before touching data written by the
 // previous kernel, so a kernel's launch, prologue and -- for the decode GEMM --
 // its first weight-tile loads overlap the previous kernel's tail. Captured
-// into CUDA graphs as programmatic edges.
+// into CUDA graphs as programmatic edges. The one exception is hx_advance (the
+// only kernel that writes seq_lens): it never triggers early, so any later
+// kernel may read seq_lens and the KV pages below it before its own wait.
 extern int g_pdl;
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
@@ -128,6 +130,23 @@ template <> __device__ __forceinline__ float from_f32<float>(float v) { return v
 template <> __device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(float v) {
   return __float2bfloat16_rn(v);
 }
+// rotate-half RoPE of the pair (x1, x2) = (x[i], x[i + hd/2]) by angle (cos c, sin s).
+// Explicit _rn ops: no FMA contraction, so every kernel that rotates (and the
+// numpy oracle, which rounds each product) produces the same bits.
+__device__ __forceinline__ float2 rope_rot(float x1, float x2, float c, float s) {
+  return make_float2(__fsub_rn(__fmul_rn(x1, c), __fmul_rn(x2, s)), __fadd_rn(__fmul_rn(x2, c), __fmul_rn(x1, s)));
+}
+// four consecutive outputs in one vector store (dst 4-element aligned)
+__device__ __forceinline__ void store4(float *dst, float a, float b, float c, float d) {
+  *reinterpret_cast<float4 *>(dst) = make_float4(a, b, c, d);
+}
+__device__ __forceinline__ void store4(__nv_bfloat16 *dst, float a, float b, float c, float d) {
+  __nv_bfloat162 lo = __floats2bfloat162_rn(a, b), hi = __floats2bfloat162_rn(c, d);
+  uint2 u;
+  u.x = *reinterpret_cast<uint32_t *>(&lo);
+  u.y = *reinterpret_cast<uint32_t *>(&hi);
+  *reinterpret_cast<uint2 *>(dst) = u;
+}
 
 // 16-byte vector of T: 4 floats or 8 bf16.
 template <typename T> struct Vec16;
@@ -197,6 +216,10 @@ __device__ __forceinline__ void named_bar_sync(int id, int threads) {
 }
 __device__ __forceinline__ void fence_barrier_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// order this thread's generic-proxy global stores before later async-proxy (TMA) reads
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),

@@ -174,8 +174,10 @@ __global__ void argmax_finalize_kernel(const long long *keys, int32_t *ids, int3
   }
 }
 
+// No early pdl_trigger: dependents launch only once seq_lens is final, so any
+// later kernel may read seq_lens (and KV pages below it) before its own
+// griddepcontrol.wait -- the decode attention prefetches pages that way.
 __global__ void advance_kernel(int32_t *seq_lens, int batch, int n) {
-  pdl_trigger();
   pdl_wait();
   const int b = threadIdx.x + blockIdx.x * blockDim.x;
   if (b < batch) seq_lens[b] += n;

@@ -97,8 +97,9 @@ __device__ __forceinline__ void epi_pair(const EpiArgs &e, int tok, int n, float
       const float inv_freq = 1.0f / powf(e.theta, (float)(2 * i) / 128.0f);
       sincosf((float)pos * inv_freq, &sn, &cs);
     }
-    y1 = lo * cs - hi * sn;
-    y2 = hi * cs + lo * sn;
+    const float2 y = rope_rot(lo, hi, cs, sn);
+    y1 = y.x;
+    y2 = y.y;
   }
   __nv_bfloat16 *dst;
   if (h < e.hq) {
@@ -442,7 +443,8 @@ __device__ __forceinline__ void emit_decode(const OutDesc od, const EpiArgs &epi
         const float inv_freq = 1.0f / powf(epi.theta, (float)(2 * i) / 128.0f);
         sincosf((float)pos[j] * inv_freq, &s, &c);
       }
-      const float y1 = rot ? lo * c - hi * s : lo, y2 = rot ? hi * c + lo * s : hi;
+      const float2 y = rot ? rope_rot(lo, hi, c, s) : make_float2(lo, hi);
+      const float y1 = y.x, y2 = y.y;
       __nv_bfloat16 *dst;
       if (h < epi.hq) {
         dst = epi.q_out + ((long)tok * epi.hq + h) * 128;
@@ -707,7 +709,6 @@ __global__ void __launch_bounds__(256)
   // one row = a cluster of SK_CL CTAs (each owns hidden / SK_CL features); the
   // RMS sum of squares is combined across the cluster through DSMEM
   pdl_trigger();
-  pdl_wait();
   __shared__ float red[8];
   __shared__ float part;
   const unsigned cr = cluster_rank();
@@ -715,7 +716,14 @@ __global__ void __launch_bounds__(256)
   const int per = hidden / SK_CL, base = (int)cr * per;
   float *xr = x + (size_t)t * hidden;
   constexpr int MAXV = 2;  // hidden <= SK_CL * 2 * 4 * 256 = 8192
-  float4 xv[MAXV], dv[MAXV];
+  float4 xv[MAXV], dv[MAXV], gv[MAXV];
+  // the gain is a weight: fetch it before waiting on the producer GEMM
+#pragma unroll
+  for (int i = 0; i < MAXV; ++i) {
+    const int n = base + (i * 256 + threadIdx.x) * 4;
+    if (out && n < base + per) gv[i] = __ldg(reinterpret_cast<const float4 *>(gain + n));
+  }
+  pdl_wait();
 #pragma unroll
   for (int i = 0; i < MAXV; ++i) {
     const int n = base + (i * 256 + threadIdx.x) * 4;
@@ -753,11 +761,8 @@ __global__ void __launch_bounds__(256)
   for (int i = 0; i < MAXV; ++i) {
     const int n = base + (i * 256 + threadIdx.x) * 4;
     if (n < base + per) {
-      const float4 g = *reinterpret_cast<const float4 *>(gain + n);
-      o[n] = from_f32<TO>((xv[i].x * inv) * g.x);
-      o[n + 1] = from_f32<TO>((xv[i].y * inv) * g.y);
-      o[n + 2] = from_f32<TO>((xv[i].z * inv) * g.z);
-      o[n + 3] = from_f32<TO>((xv[i].w * inv) * g.w);
+      const float4 g = gv[i];
+      store4(o + n, (xv[i].x * inv) * g.x, (xv[i].y * inv) * g.y, (xv[i].z * inv) * g.z, (xv[i].w * inv) * g.w);
     }
   }
 }

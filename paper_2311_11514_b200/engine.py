@@ -26,6 +26,7 @@ pointers, issues collectives and sequences launches.
 from __future__ import annotations
 
 import math
+import os
 import time
 from dataclasses import dataclass
 
@@ -47,7 +48,6 @@ def fused_epilogues() -> tuple[bool, bool]:
     tensor-core path; off by default (measured slower than the separate kernels at
     7B batch 16), HX_FUSE_SWIGLU=1 / HX_FUSE_ROPE=1 enable them.
     The bf16 oracle takes the same pair (rounding points differ between the two)."""
-    import os
     return (os.environ.get("HX_FUSE_SWIGLU", "0") == "1", os.environ.get("HX_FUSE_ROPE", "0") == "1")
 
 
@@ -173,6 +173,12 @@ class RankExecutor:
         want_swiglu, want_rope = fused_epilogues()
         self.fuse_swiglu = tc and want_swiglu and inter_r % 64 == 0
         self.fuse_rope = tc and want_rope and cfg.head_dim == 128
+        # decode RoPE + KV append inside the TMA attention kernel (bit-identical to
+        # the separate kernels); HX_FUSE_ROPE_ATTN=0 selects rope_kv_append + attn_decode
+        self.rope_in_attn = (self.device.type == "cuda" and self.k is _ops and not self.fuse_rope
+                             and _ops.decode_rope_fusable(dtype, cfg.head_dim, page_size, cfg.num_heads // role.tp,
+                                                          cfg.num_kv_heads // role.tp)
+                             and os.environ.get("HX_FUSE_ROPE_ATTN", "1") != "0")
         if pack_weights and dtype == torch.bfloat16 and self.device.type == "cuda":
             # tile-contiguous layout for the weight-streaming GEMM (hx_pack_weight)
             for lw in weights["layers"]:
@@ -237,7 +243,11 @@ class RankExecutor:
         if li == 0:  # input norm of the stage's first layer (x arrived raw)
             k.rmsnorm(self.x, lw["ln_attn"], self.h, n_tok, cfg.rms_eps)
         kc, vc = self.kv.k[li], self.kv.v[li]
-        if self.fuse_rope and not prefill_len:  # decode: QKV GEMM with RoPE + KV append in its epilogue
+        if self.rope_in_attn and not prefill_len:  # decode: RoPE + KV append inside the attention kernel
+            k.linear(lw["wqkv"], self.h, self.qkv, n_tok, self.lin_ws)
+            k.attn_decode_rope_append(self.qkv, kc, vc, self.kv.block_table, self.kv.seq_lens, self.attn, n_tok,
+                                      self.hq, self.hkv, self.hd, self.max_ctx, cfg.rope_theta, self.attn_ws)
+        elif self.fuse_rope and not prefill_len:  # decode: QKV GEMM with RoPE + KV append in its epilogue
             k.linear_rope_kv(lw["wqkv"], self.h, self.q, kc, vc, self.kv.block_table, self.kv.seq_lens, n_tok,
                              prefill_len, self.hq, self.hkv, cfg.rope_theta, self.lin_ws, self.rope_tab)
         else:
@@ -247,7 +257,7 @@ class RankExecutor:
         if prefill_len:
             k.attn_prefill(self.q, kc, vc, self.kv.block_table, self.kv.seq_lens, self.attn,
                            n_tok // prefill_len, prefill_len, self.hq, self.hkv, self.hd)
-        else:
+        elif not self.rope_in_attn:
             k.attn_decode(self.q, kc, vc, self.kv.block_table, self.kv.seq_lens, self.attn, n_tok,
                           self.hq, self.hkv, self.hd, self.max_ctx, self.attn_ws)
         # TP=1 decode: the O/down GEMMs leave split tiles as partials and the

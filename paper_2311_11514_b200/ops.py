@@ -52,6 +52,7 @@ _SIGS = {
     "hx_rope_kv_append": ([_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _F, _P], _I),
     "hx_attn_decode_paged": ([_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _SZ, _P], _I),
     "hx_attn_decode_workspace": ([_I, _I, _I, _I, _I], _SZ),
+    "hx_attn_decode_rope_append": ([_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _F, _P, _SZ, _P], _I),
     "hx_attn_prefill": ([_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P], _I),
     "hx_advance": ([_P, _I, _I, _P], _I),
     "hx_argmax_partial": ([_P, _P, _I, _I, _I, _I, _P], _I),
@@ -261,6 +262,26 @@ def attn_decode(q, k_cache, v_cache, block_table, seq_lens, o, batch, hq, hkv, h
                                        block_table.shape[1], max_ctx, _p(ws),
                                        0 if ws is None else ws.numel() * ws.element_size(), _stream()),
            "hx_attn_decode_paged")
+
+
+def decode_rope_fusable(dtype, hd, page, hq, hkv) -> bool:
+    """Whether hx_attn_decode_rope_append takes this shape (bf16, hd 128,
+    page 64, GQA group in {1, 2, 4, 8, 16}; HX_ATTN_TMA not 0)."""
+    import os
+    return (dtype == torch.bfloat16 and hd == 128 and page == 64 and hq % hkv == 0
+            and hq // hkv in (1, 2, 4, 8, 16) and os.environ.get("HX_ATTN_TMA", "1") != "0")
+
+
+def attn_decode_rope_append(qkv, k_cache, v_cache, block_table, seq_lens, o, batch, hq, hkv, hd, max_ctx,
+                            theta, workspace=None):
+    """RoPE + KV append of the new token fused into decode attention
+    (hx_attn_decode_rope_append); q is read un-rotated from the qkv rows."""
+    ws = workspace
+    _check(load().hx_attn_decode_rope_append(_p(qkv), _p(k_cache), _p(v_cache), _p(block_table), _p(seq_lens),
+                                             _p(o), dtype_code(qkv.dtype), batch, hq, hkv, hd, k_cache.shape[2],
+                                             block_table.shape[1], max_ctx, theta, _p(ws),
+                                             0 if ws is None else ws.numel() * ws.element_size(), _stream()),
+           "hx_attn_decode_rope_append")
 
 
 def attn_prefill(q, k_cache, v_cache, block_table, seq_lens, o, batch, s, hq, hkv, hd):

@@ -318,6 +318,48 @@ def test_rope_append_and_decode_attention(dt, hq, hkv, hd, ctx, page):
     assert torch.equal(o, o2)
 
 
+@pytest.mark.parametrize("hq,hkv,ctx,b", [(32, 32, 600, 3), (32, 32, 575, 8), (16, 2, 1100, 3), (64, 8, 300, 2),
+                                          (16, 1, 2, 3), (8, 8, 63, 1), (8, 4, 128, 2), (32, 2, 1279, 1)])
+def test_decode_rope_append_fused_bit_identical(hq, hkv, ctx, b):
+    """hx_attn_decode_rope_append == hx_rope_kv_append + hx_attn_decode_paged, bit for
+    bit (q, the appended K/V page slots and the attention output), with per-sequence
+    lengths that put the new token at page starts, page ends and mid-page."""
+    dt, hd, page = torch.bfloat16, 128, 64
+    kc, vc, bt, g = _paged_setup(dt, b, hq, hkv, hd, page, ctx + 1)
+    n = (hq + 2 * hkv) * hd
+    hist = torch.randn(b * ctx, n, device=DEV, generator=g).to(dt)
+    seq = torch.zeros(b, dtype=torch.int32, device=DEV)
+    ops.rope_kv_append(hist, torch.empty(b * ctx, hq * hd, device=DEV, dtype=dt), kc, vc, bt, seq, b * ctx, ctx,
+                       hq, hkv, hd, 10000.0)
+    lens = [max(0, ctx - 64 * i - (i % 3)) for i in range(b)]
+    seq.copy_(torch.tensor(lens, dtype=torch.int32))
+    new = torch.randn(b, n, device=DEV, generator=g).to(dt)
+    ws = torch.zeros(ops.attn_decode_workspace(b, hq, hkv, hd, ctx + 1) // 4 + 64, dtype=torch.int32, device=DEV)
+    k2, v2 = kc.clone(), vc.clone()
+    q = torch.empty(b, hq * hd, device=DEV, dtype=dt)
+    o_sep = torch.empty(b, hq * hd, device=DEV, dtype=dt)
+    ops.rope_kv_append(new, q, kc, vc, bt, seq, b, 0, hq, hkv, hd, 10000.0)
+    ops.attn_decode(q, kc, vc, bt, seq, o_sep, b, hq, hkv, hd, ctx + 1, ws)
+    o_fused = torch.empty_like(o_sep)
+    ops.attn_decode_rope_append(new, k2, v2, bt, seq, o_fused, b, hq, hkv, hd, ctx + 1, 10000.0, ws)
+    torch.cuda.synchronize()
+    assert torch.equal(k2, kc) and torch.equal(v2, vc)
+    assert torch.equal(o_fused, o_sep)
+
+
+def test_decode_rope_append_fused_unsupported_shapes():
+    assert not ops.decode_rope_fusable(torch.float32, 128, 64, 8, 8)
+    assert not ops.decode_rope_fusable(torch.bfloat16, 64, 64, 8, 8)
+    assert not ops.decode_rope_fusable(torch.bfloat16, 128, 16, 8, 8)
+    dt = torch.bfloat16
+    kc, vc, bt, _ = _paged_setup(dt, 1, 4, 4, 128, 16, 32)
+    qkv = torch.zeros(1, 12 * 128, device=DEV, dtype=dt)
+    seq = torch.zeros(1, dtype=torch.int32, device=DEV)
+    with pytest.raises(ops.HxError):
+        ops.attn_decode_rope_append(qkv, kc, vc, bt, seq, torch.empty(1, 4 * 128, device=DEV, dtype=dt),
+                                    1, 4, 4, 128, 32, 10000.0)
+
+
 @pytest.mark.parametrize("dt", [torch.float32, torch.bfloat16])
 @pytest.mark.parametrize("hq,hkv,hd,s", [(8, 8, 32, 64), (4, 4, 128, 200), (8, 2, 128, 130), (2, 2, 64, 1),
                                           (4, 4, 64, 257), (2, 1, 128, 64), (1, 1, 128, 513)])
