@@ -154,6 +154,20 @@ int hx_tp_allreduce_residual_rmsnorm(float *x, const float *const *parts, int *c
                                      const float *gain, void *out, int out_dtype, int n_tok,
                                      int hidden, float eps, hx_stream_t stream);
 
+/* Push (one-shot, flag-free) variant of the same all-reduce: each rank stores
+ * its partial row into every peer's inbox over NVLink and polls its own inbox
+ * for the peers' rows (sentinel -0.0f until the data lands). inboxes[r] = rank
+ * r's inbox of hx_tp_inbox_bytes(tp, max_tok, hidden) bytes (peer-mapped; own
+ * local), armed once with hx_tp_inbox_init; own_part = this rank's partial
+ * [n_tok][hidden]; state = this rank's int[2] call counter (zeroed). Same
+ * result bits as hx_tp_allreduce_residual_rmsnorm. */
+size_t hx_tp_inbox_bytes(int tp, int max_tok, int hidden);
+int hx_tp_inbox_init(void *inbox, int tp, int max_tok, int hidden, hx_stream_t stream);
+int hx_tp_allreduce_push_residual_rmsnorm(float *x, const float *own_part, float *const *inboxes,
+                                          int rank, int tp, int max_tok, int *state,
+                                          const float *gain, void *out, int out_dtype, int n_tok,
+                                          int hidden, float eps, hx_stream_t stream);
+
 /* out[t, j] = silu(gu[t, j]) * gu[t, inter + j], j < inter */
 int hx_swiglu(const void *gu, void *out, int dtype, int n_tok, int inter,
               hx_stream_t stream);

@@ -112,6 +112,135 @@ __global__ void __launch_bounds__(1024)
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Push ("one-shot, flag-free") variant. The pull kernel above pays three
+// dependent NVLink trips per call (flag store -> peer flag observed -> remote
+// loads). Here every rank PUSHES its partial row into every peer's inbox with
+// plain remote stores and each receiver polls its own LOCAL inbox until the
+// data itself is there: an inbox element holds the sentinel -0.0f (0x80000000)
+// until a peer's store lands (pushed values are sanitised -0.0 -> +0.0, which
+// cannot change any sum). One one-way NVLink trip per call, no fences.
+// Inbox per rank: [3 buffers][tp senders][max_tok][hidden] fp32; call k uses
+// buffer k % 3 and re-arms buffer (k + 2) % 3 (consumed at call k - 1; no peer
+// can write it again before call k + 2, which needs this rank's call k + 1
+// data). The call counter lives in state[0] and is bumped by the last CTA.
+struct ArInbox {
+  float *box[kMaxTP];  // rank r's inbox (peer-mapped; own = local)
+};
+
+constexpr uint32_t kSentinel = 0x80000000u;
+
+__device__ __forceinline__ uint4 ld_volatile_u4(const void *p) {
+  uint4 v;
+  asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ bool has_sentinel(const uint4 &v) {
+  return v.x == kSentinel || v.y == kSentinel || v.z == kSentinel || v.w == kSentinel;
+}
+__device__ __forceinline__ float4 sanitize(float4 v) {  // -0.0 -> +0.0 (bitwise), value-preserving
+  v.x += 0.0f; v.y += 0.0f; v.z += 0.0f; v.w += 0.0f;
+  return v;
+}
+
+template <typename TO>
+__global__ void __launch_bounds__(1024)
+    tp_ar_push_rmsnorm_kernel(float *x, const float *own, ArInbox ib, int rank, int tp, int max_tok, int n_tok,
+                              int *state, const float *gain, TO *out, int hidden, float eps) {
+  pdl_trigger();
+  pdl_wait();  // this rank's partial (previous kernel) is complete
+  __shared__ float red[32];
+  const int t = blockIdx.x;
+  const int call = *(volatile int *)state;
+  const int buf = call % 3, rearm = (call + 2) % 3;
+  const size_t row = (size_t)hidden;
+  float *mine = ib.box[rank];
+  constexpr int MAXV = 2;  // hidden <= 8192
+  float4 p[MAXV];
+  // 1. push my partial row t to every peer (remote stores; nothing waits on them here)
+#pragma unroll
+  for (int i = 0; i < MAXV; ++i) {
+    const int n = (i * 1024 + threadIdx.x) * 4;
+    if (n >= hidden) continue;
+    p[i] = sanitize(__ldcs(reinterpret_cast<const float4 *>(own + (size_t)t * row + n)));
+    for (int r = 0; r < tp; ++r)
+      if (r != rank)
+        *reinterpret_cast<float4 *>(ib.box[r] + (((size_t)buf * tp + rank) * max_tok + t) * row + n) = p[i];
+  }
+  // 2. re-arm the buffer consumed by the previous call (all rows this CTA owns)
+  const float4 s4 = make_float4(__uint_as_float(kSentinel), __uint_as_float(kSentinel), __uint_as_float(kSentinel),
+                                __uint_as_float(kSentinel));
+  for (int rr = t; rr < max_tok; rr += n_tok)
+#pragma unroll
+    for (int i = 0; i < MAXV; ++i) {
+      const int n = (i * 1024 + threadIdx.x) * 4;
+      if (n >= hidden) continue;
+      for (int r = 0; r < tp; ++r)
+        if (r != rank) *reinterpret_cast<float4 *>(mine + (((size_t)rearm * tp + r) * max_tok + rr) * row + n) = s4;
+    }
+  // 3. poll my inbox for every peer's row t, sum in rank order (bitwise identical on all ranks)
+  float ss = 0.f;
+  float4 v[MAXV];
+#pragma unroll
+  for (int i = 0; i < MAXV; ++i) {
+    const int n = (i * 1024 + threadIdx.x) * 4;
+    if (n >= hidden) continue;
+    float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int r = 0; r < tp; ++r) {
+      float4 q = p[i];
+      if (r != rank) {
+        const float *src = mine + (((size_t)buf * tp + r) * max_tok + t) * row + n;
+        uint4 u = ld_volatile_u4(src);
+        for (uint32_t spins = 0; has_sentinel(u); ++spins) {
+          if (spins > (1u << 26)) __trap();  // a peer never arrived: fail loudly, never hang
+          u = ld_volatile_u4(src);
+        }
+        q = make_float4(__uint_as_float(u.x), __uint_as_float(u.y), __uint_as_float(u.z), __uint_as_float(u.w));
+      }
+      sum.x += q.x; sum.y += q.y; sum.z += q.z; sum.w += q.w;
+    }
+    float4 acc = *reinterpret_cast<const float4 *>(x + (size_t)t * row + n);
+    acc.x += sum.x; acc.y += sum.y; acc.z += sum.z; acc.w += sum.w;
+    *reinterpret_cast<float4 *>(x + (size_t)t * row + n) = acc;
+    v[i] = acc;
+    ss += acc.x * acc.x + acc.y * acc.y + acc.z * acc.z + acc.w * acc.w;
+  }
+  if (out) {
+    ss = warp_sum(ss);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    float tot = 0.f;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) tot += red[i];
+    const float inv = 1.0f / sqrtf(tot / (float)hidden + eps);
+#pragma unroll
+    for (int i = 0; i < MAXV; ++i) {
+      const int n = (i * 1024 + threadIdx.x) * 4;
+      if (n >= hidden) continue;
+      const float4 g = *reinterpret_cast<const float4 *>(gain + n);
+      TO *o = out + (size_t)t * row + n;
+      o[0] = from_f32<TO>((v[i].x * inv) * g.x);
+      o[1] = from_f32<TO>((v[i].y * inv) * g.y);
+      o[2] = from_f32<TO>((v[i].z * inv) * g.z);
+      o[3] = from_f32<TO>((v[i].w * inv) * g.w);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int done = atomicAdd(state + 1, 1);
+    if (done == (int)gridDim.x - 1) {
+      state[1] = 0;
+      *(volatile int *)state = call + 1;
+    }
+  }
+}
+
+__global__ void fill_u32_kernel(uint32_t *p, size_t n, uint32_t v) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
 }  // namespace hx
 
 using namespace hx;
@@ -163,4 +292,33 @@ extern "C" int hx_tp_allreduce_residual_rmsnorm(float *x, const float *const *pa
                   site_state, gain, (__nv_bfloat16 *)out, hidden, eps);
   return launch(tp_ar_rmsnorm_kernel<float>, dim3(n_tok), dim3(1024), 0, st, x, p, rank, tp, site, max_tok,
                 site_state, gain, (float *)out, hidden, eps);
+}
+
+extern "C" size_t hx_tp_inbox_bytes(int tp, int max_tok, int hidden) {
+  return (size_t)3 * tp * max_tok * hidden * sizeof(float);
+}
+
+extern "C" int hx_tp_inbox_init(void *inbox, int tp, int max_tok, int hidden, hx_stream_t stream) {
+  if (!inbox || tp < 1 || max_tok < 1 || hidden < 1) return HX_ERR_ARG;
+  const size_t n = hx_tp_inbox_bytes(tp, max_tok, hidden) / 4;
+  fill_u32_kernel<<<296, 256, 0, as_stream(stream)>>>((uint32_t *)inbox, n, kSentinel);
+  return launch_status();
+}
+
+extern "C" int hx_tp_allreduce_push_residual_rmsnorm(float *x, const float *own_part, float *const *inboxes, int rank,
+                                                     int tp, int max_tok, int *state, const float *gain, void *out,
+                                                     int out_dtype, int n_tok, int hidden, float eps,
+                                                     hx_stream_t stream) {
+  if (n_tok == 0) return 0;
+  if (!x || !own_part || !inboxes || !state || tp < 1 || tp > kMaxTP || rank < 0 || rank >= tp ||
+      n_tok > max_tok || hidden % 4 || hidden > 8192 || (out && !gain))
+    return HX_ERR_ARG;
+  ArInbox ib{};
+  for (int r = 0; r < tp; ++r) ib.box[r] = inboxes[r];
+  cudaStream_t st = as_stream(stream);
+  if (out_dtype == HX_BF16)
+    return launch(tp_ar_push_rmsnorm_kernel<__nv_bfloat16>, dim3(n_tok), dim3(1024), 0, st, x, own_part, ib, rank,
+                  tp, max_tok, n_tok, state, gain, (__nv_bfloat16 *)out, hidden, eps);
+  return launch(tp_ar_push_rmsnorm_kernel<float>, dim3(n_tok), dim3(1024), 0, st, x, own_part, ib, rank, tp,
+                max_tok, n_tok, state, gain, (float *)out, hidden, eps);
 }

@@ -48,6 +48,10 @@ _SIGS = {
     "hx_ipc_close": ([_P], _I),
     "hx_tp_allreduce_residual_rmsnorm": ([_P, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p),
                                           _I, _I, _I, _I, _P, _P, _P, _I, _I, _I, _F, _P], _I),
+    "hx_tp_inbox_bytes": ([_I, _I, _I], _SZ),
+    "hx_tp_inbox_init": ([_P, _I, _I, _I, _P], _I),
+    "hx_tp_allreduce_push_residual_rmsnorm": ([_P, _P, ctypes.POINTER(ctypes.c_void_p), _I, _I, _I, _P, _P, _P, _I,
+                                               _I, _I, _F, _P], _I),
     "hx_swiglu": ([_P, _P, _I, _I, _I, _P], _I),
     "hx_rope_kv_append": ([_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _F, _P], _I),
     "hx_attn_decode_paged": ([_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _SZ, _P], _I),
@@ -311,22 +315,40 @@ def kv_bytes(dtype, layers, num_blocks, hkv_rank, page, hd) -> int:
 
 # ---------------------------------------------------------------- NVLink TP all-reduce
 class PeerAllReduce:
-    """Per-rank state of the fused NVLink all-reduce (hx_tp_allreduce_residual_rmsnorm):
-    two fp32 partial slots and a flag array in cudaIpc-exported memory, mapped on
-    every rank of the TP group (handles exchanged once over ``group``)."""
+    """Per-rank state of the fused NVLink all-reduce + residual + RMSNorm of a
+    TP>1 decode step, in cudaIpc-exported memory mapped on every rank of the TP
+    group (handles exchanged once over ``group``):
 
-    def __init__(self, rank: int, tp: int, max_tok: int, hidden: int, sites: int, group, dist):
+    * ``mode='push'`` (default, hx_tp_allreduce_push_residual_rmsnorm): each
+      rank stores its partial into every peer's sentinel-armed inbox and polls
+      its own -- one one-way NVLink trip per call;
+    * ``mode='pull'`` (hx_tp_allreduce_residual_rmsnorm): epoch flags, then
+      peer loads of every rank's partial slot.
+    Both sum in rank order and give identical bits."""
+
+    def __init__(self, rank: int, tp: int, max_tok: int, hidden: int, sites: int, group, dist, mode: str | None = None):
+        import os
         lib = load()
+        self.mode = mode or os.environ.get("HX_AR_MODE", "push")
+        if self.mode not in ("push", "pull"):
+            raise HxError(f"unknown all-reduce mode {self.mode!r}")
         self.rank, self.tp, self.max_tok, self.hidden, self.sites = rank, tp, max_tok, hidden, sites
         slot_bytes = max_tok * hidden * 4
-        flag_bytes = sites * max_tok * 8 * 4
+        bufs = [("slot0", slot_bytes), ("slot1", slot_bytes)]
+        if self.mode == "pull":
+            bufs.append(("flags", sites * max_tok * 8 * 4))
+        else:
+            bufs.append(("inbox", int(lib.hx_tp_inbox_bytes(tp, max_tok, hidden))))
         self._own = []
         ptrs = {}
-        for name, nbytes in (("slot0", slot_bytes), ("slot1", slot_bytes), ("flags", flag_bytes)):
+        for name, nbytes in bufs:
             p = ctypes.c_void_p()
             _check(lib.hx_ipc_alloc(ctypes.byref(p), nbytes), "hx_ipc_alloc")
             self._own.append(p.value)
             ptrs[name] = p.value
+        if self.mode == "push":
+            _check(lib.hx_tp_inbox_init(ptrs["inbox"], tp, max_tok, hidden, None), "hx_tp_inbox_init")
+            torch.cuda.synchronize()
         handles = {}
         for name, p in ptrs.items():
             h = ctypes.create_string_buffer(64)
@@ -340,7 +362,7 @@ class PeerAllReduce:
             for name in ptrs:
                 if r == rank:
                     self.peer[name][r] = ptrs[name]
-                else:
+                elif name in ("flags", "inbox") or self.mode == "pull":
                     q = ctypes.c_void_p()
                     _check(lib.hx_ipc_open(gathered[r][name], ctypes.byref(q)), "hx_ipc_open")
                     self.peer[name][r] = q.value
@@ -356,6 +378,12 @@ class PeerAllReduce:
 
     def allreduce_residual_rmsnorm(self, x, site, gain, out, n_tok, eps):
         lib = load()
+        if self.mode == "push":
+            _check(lib.hx_tp_allreduce_push_residual_rmsnorm(
+                _p(x), self.peer[f"slot{site % 2}"][self.rank], self._arr["inbox"], self.rank, self.tp, self.max_tok,
+                _p(self.site_state), _p(gain), _p(out), dtype_code(out.dtype) if out is not None else HX_F32,
+                n_tok, self.hidden, eps, _stream()), "hx_tp_allreduce_push_residual_rmsnorm")
+            return
         _check(lib.hx_tp_allreduce_residual_rmsnorm(
             _p(x), self._arr[f"slot{site % 2}"], self._arr["flags"], self.rank, self.tp, site, self.max_tok,
             _p(self.site_state), _p(gain), _p(out), dtype_code(out.dtype) if out is not None else HX_F32,

@@ -72,3 +72,19 @@ def test_nccl_asymmetric_21_fp32_graphs():
 @pytest.mark.skipif(_gpus() < 4, reason="needs >= 4 GPUs")
 def test_nccl_asymmetric_211_bf16_graphs():
     _run(4, ["--plan", "2,1,1", "--layers", "2,1,1", "--dtype", "bf16", "--graphs"])
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(_gpus() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("n", [2, 4])
+def test_peer_allreduce_push_equals_pull(n):
+    """The flag-free push all-reduce gives the same bits as the flag/pull one,
+    and the residual stays bitwise replicated across the TP ranks."""
+    if _gpus() < n:
+        pytest.skip(f"needs {n} GPUs")
+    env = dict(os.environ, OMP_NUM_THREADS="2")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={_port()}", str(ROOT / "tools" / "ar_bench.py"), "--check"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert r.stdout.count("push==pull: True, replicated: True") == n, r.stdout
