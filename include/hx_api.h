@@ -168,6 +168,23 @@ int hx_tp_allreduce_push_residual_rmsnorm(float *x, const float *own_part, float
                                           const float *gain, void *out, int out_dtype, int n_tok,
                                           int hidden, float eps, hx_stream_t stream);
 
+/* ---- Inter-stage reshard over NVLink P2P (decode hand-off and token return).
+ * Replaces the leader send + broadcast of PAPER.md:197 (modelled by
+ * pp_comm_cost, costs.py:150-165): receiver r' of stage j+1 owns an inbox that
+ * sender r' mod TP_j stores into directly (hx_handoff_push), and it polls the
+ * inbox in place (hx_handoff_pull) -- 32-bit words armed with the sentinel
+ * 0x80000000 by hx_handoff_inbox_init; pushed words equal to it travel as 0.
+ * inbox = hx_handoff_inbox_bytes(max_words) bytes from hx_ipc_alloc, mapped on
+ * the sender with hx_ipc_open; max_words % 4 == 0; words <= max_words; each
+ * side's state = its own zeroed int[2] call counter. Both are graph-capturable
+ * and need no host synchronisation; waits are bounded (trap, not hang). */
+size_t hx_handoff_inbox_bytes(size_t max_words);
+int hx_handoff_inbox_init(void *inbox, size_t max_words, hx_stream_t stream);
+int hx_handoff_push(const void *src, void *const *dst_inboxes, int n_dst, size_t words,
+                    size_t max_words, int *state, hx_stream_t stream);
+int hx_handoff_pull(void *dst, void *inbox, size_t words, size_t max_words, int *state,
+                    hx_stream_t stream);
+
 /* out[t, j] = silu(gu[t, j]) * gu[t, inter + j], j < inter */
 int hx_swiglu(const void *gu, void *out, int dtype, int n_tok, int inter,
               hx_stream_t stream);

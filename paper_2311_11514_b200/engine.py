@@ -355,22 +355,36 @@ class StageDriver:
         for e in self.execs:
             e.finalize()
 
-    def send_hidden(self, n_tok):
+    def send_hidden(self, n_tok, decode: bool = False):
         for e in self.execs:
+            if decode and e.p2p_send:      # NVLink P2P store into each receiver's inbox
+                for link in e.p2p_send:
+                    link.push(e.x[:n_tok])
+                continue
             for dst in e.role.send_to:
                 self.comm.send(e.x[:n_tok], e.role.device, dst)
 
-    def recv_hidden(self, n_tok):
+    def recv_hidden(self, n_tok, decode: bool = False):
         for e in self.execs:
+            if decode and e.p2p_recv is not None:
+                e.p2p_recv.pull(e.x[:n_tok])
+                continue
             self.comm.recv(e.x[:n_tok], e.role.recv_from, e.role.device)
 
     def send_ids(self):
         for e in self.execs:
+            if e.ids_send:
+                for link in e.ids_send:
+                    link.push(e.ids)
+                continue
             for dst in e.role.ids_send_to:
                 self.comm.send(e.ids, e.role.device, dst)
 
     def recv_ids(self):
         for e in self.execs:
+            if e.ids_recv is not None:
+                e.ids_recv.pull(e.ids)
+                continue
             self.comm.recv(e.ids, e.role.ids_recv_from, e.role.device)
 
 
@@ -431,6 +445,12 @@ class Engine:
                 if e.role.tp > 1:  # fused NVLink all-reduce for the decode step
                     e.par = _ops.PeerAllReduce(e.role.tp_rank, e.role.tp, batch, cfg.hidden_dim, 2 * e.n_layers,
                                                self.comm.groups[e.role.tp_group], self.comm.dist)
+        for e in execs:
+            e.p2p_send, e.p2p_recv, e.ids_send, e.ids_recv = [], None, [], None
+        self._p2p = (self.comm.kind == "dist" and self.device.type == "cuda" and kernels is None
+                     and self.num_stages > 1 and os.environ.get("HX_P2P", "1") != "0")
+        if self._p2p:
+            self._setup_p2p(execs)
         self.drivers = []
         for j in sorted({r.stage for r in local}):
             self.drivers.append(StageDriver([e for e in execs if e.role.stage == j], self.comm, j))
@@ -440,6 +460,33 @@ class Engine:
         self._graph_key = None
         self._graph_launches = []
         self._replayed = 0
+
+    def _setup_p2p(self, execs):
+        """NVLink P2P links for the decode hand-offs (hidden j -> j+1, ids
+        last -> 0), created in one global order so the pairwise handle
+        exchanges of every rank line up."""
+        links = []
+        for r in self.roles:
+            links += [("hidden", r.device, dst) for dst in r.send_to]
+            links += [("ids", r.device, dst) for dst in r.ids_send_to]
+        mine = {e.role.device: e for e in execs}
+        for kind, src, dst in sorted(links):
+            me = src if src in mine else dst if dst in mine else None
+            if me is None:
+                continue
+            words = self.batch * (self.cfg.hidden_dim if kind == "hidden" else 1)
+            link = _ops.P2PLink(src, dst, me, words, self.comm.pairs[(min(src, dst), max(src, dst))],
+                                self.comm.dist)
+            e = mine[me]
+            if kind == "hidden":
+                if me == src:
+                    e.p2p_send.append(link)
+                else:
+                    e.p2p_recv = link
+            elif me == src:
+                e.ids_send.append(link)
+            else:
+                e.ids_recv = link
 
     # ---------------------------------------------------------------- steps
     def _prefill(self, b, s):
@@ -472,7 +519,29 @@ class Engine:
             if d.stage == 0:
                 d.recv_ids()
 
+    def _decode_full(self, d: StageDriver, b):
+        """One local stage's whole decode step in P2P mode: token ids in
+        (stage 0) / out (last stage), hidden in, compute, hidden out -- all
+        device-side, so it is captured as one graph per step."""
+        if d.stage == self.num_stages - 1:
+            d.send_ids()
+        if d.stage == 0:
+            d.recv_ids()
+        if d.stage > 0:
+            d.recv_hidden(b, decode=True)
+        self._decode_compute(d, b)
+        if d.stage < self.num_stages - 1:
+            d.send_hidden(b, decode=True)
+
     def _decode_step(self, b, graphs=None):
+        if self._p2p:
+            for i, d in enumerate(self.drivers):
+                if graphs is not None:
+                    graphs[i].replay()
+                    self._replayed += self._graph_launches[i]
+                else:
+                    self._decode_full(d, b)
+            return
         self._return_ids()
         for i, d in enumerate(self.drivers):
             if d.stage > 0:
@@ -497,7 +566,10 @@ class Engine:
             n0 = self._launch_count()
             # thread_local: the NCCL watchdog thread keeps querying events during capture
             with torch.cuda.graph(g, capture_error_mode="thread_local"):
-                self._decode_compute(d, b)
+                if self._p2p:
+                    self._decode_full(d, b)
+                else:
+                    self._decode_compute(d, b)
             counts.append(self._launch_count() - n0)
             graphs.append(g)
         self._graphs, self._graph_key, self._graph_launches = graphs, key, counts
@@ -542,13 +614,7 @@ class Engine:
                     if e.role.is_first:
                         e.prompt[:b * s].copy_(torch.from_numpy(prompt.reshape(-1)))
                 self._prefill(b, s)
-                self._return_ids()
-                for d in self.drivers:
-                    if d.stage > 0:
-                        d.recv_hidden(b)
-                    self._decode_compute(d, b)
-                    if d.stage < self.num_stages - 1:
-                        d.send_hidden(b)
+                self._decode_step(b, None)
                 torch.cuda.synchronize(self.device)
                 self._capture(b)
         graphs = self._graphs if (cuda and self.use_graphs and not return_logits) else None

@@ -52,6 +52,10 @@ _SIGS = {
     "hx_tp_inbox_init": ([_P, _I, _I, _I, _P], _I),
     "hx_tp_allreduce_push_residual_rmsnorm": ([_P, _P, ctypes.POINTER(ctypes.c_void_p), _I, _I, _I, _P, _P, _P, _I,
                                                _I, _I, _F, _P], _I),
+    "hx_handoff_inbox_bytes": ([_SZ], _SZ),
+    "hx_handoff_inbox_init": ([_P, _SZ, _P], _I),
+    "hx_handoff_push": ([_P, ctypes.POINTER(ctypes.c_void_p), _I, _SZ, _SZ, _P, _P], _I),
+    "hx_handoff_pull": ([_P, _P, _SZ, _SZ, _P, _P], _I),
     "hx_swiglu": ([_P, _P, _I, _I, _I, _P], _I),
     "hx_rope_kv_append": ([_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _F, _P], _I),
     "hx_attn_decode_paged": ([_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _SZ, _P], _I),
@@ -388,6 +392,49 @@ class PeerAllReduce:
             _p(x), self._arr[f"slot{site % 2}"], self._arr["flags"], self.rank, self.tp, site, self.max_tok,
             _p(self.site_state), _p(gain), _p(out), dtype_code(out.dtype) if out is not None else HX_F32,
             n_tok, self.hidden, eps, _stream()), "hx_tp_allreduce_residual_rmsnorm")
+
+
+# ---------------------------------------------------------------- NVLink P2P stage hand-off
+class P2PLink:
+    """One directed decode hand-off link (sender device -> receiver device) of
+    the inter-stage reshard (hx_handoff_push / hx_handoff_pull): the receiver
+    owns a sentinel-armed inbox in cudaIpc memory, the sender maps it. Built
+    collectively by the two ranks over their 2-rank ``group``."""
+
+    def __init__(self, src: int, dst: int, me: int, max_words: int, group, dist):
+        lib = load()
+        self.src, self.dst, self.me = src, dst, me
+        self.max_words = (max_words + 3) // 4 * 4
+        self.state = torch.zeros(2, dtype=torch.int32, device="cuda")
+        handle = None
+        self._own = self._peer = None
+        if me == dst:
+            p = ctypes.c_void_p()
+            _check(lib.hx_ipc_alloc(ctypes.byref(p), int(lib.hx_handoff_inbox_bytes(self.max_words))), "hx_ipc_alloc")
+            self._own = p.value
+            _check(lib.hx_handoff_inbox_init(self._own, self.max_words, None), "hx_handoff_inbox_init")
+            torch.cuda.synchronize()
+            h = ctypes.create_string_buffer(64)
+            _check(lib.hx_ipc_handle(self._own, h), "hx_ipc_handle")
+            handle = h.raw
+        got = [None, None]
+        dist.all_gather_object(got, handle, group=group)
+        if me == src:
+            q = ctypes.c_void_p()
+            _check(lib.hx_ipc_open(next(h for h in got if h is not None), ctypes.byref(q)), "hx_ipc_open")
+            self._peer = q.value
+        dist.barrier(group=group)
+
+    def push(self, t: torch.Tensor):
+        """Sender: store ``t`` (contiguous, 32-bit words) into the receiver's inbox."""
+        arr = (ctypes.c_void_p * 1)(self._peer)
+        _check(load().hx_handoff_push(_p(t), arr, 1, t.numel() * t.element_size() // 4, self.max_words,
+                                      _p(self.state), _stream()), "hx_handoff_push")
+
+    def pull(self, t: torch.Tensor):
+        """Receiver: wait for this hand-off's data and copy it into ``t``."""
+        _check(load().hx_handoff_pull(_p(t), self._own, t.numel() * t.element_size() // 4, self.max_words,
+                                      _p(self.state), _stream()), "hx_handoff_pull")
 
 
 def _tensor_at(ptr: int, shape) -> torch.Tensor:

@@ -27,6 +27,7 @@ from paper_2311_11514_b200.plan import simple_plan
 
 
 def main():
+    os.environ.setdefault("HX_P2P", "0")  # solo stage replays cannot wait on P2P hand-offs
     ap = argparse.ArgumentParser()
     ap.add_argument("--model", default="llama2-70b")
     ap.add_argument("--plan", default="2,1,1")
