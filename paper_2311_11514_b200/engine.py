@@ -236,6 +236,19 @@ class RankExecutor:
         self.par = None          # ops.PeerAllReduce when TP>1 ranks run in separate processes
         self._peer_now = False
         self.attn_ws = torch.zeros(max(self.attn_ws_bytes, 256) // 4 + 64, dtype=torch.int32, device=dev)
+        self._x_full = self.x
+        self.bt, self.sl = self.kv.block_table, self.kv.seq_lens   # the current micro-batch's sequences
+
+    def window(self, seq0: int, seqs: int, seq_len: int):
+        """Point the residual stream and the KV tables at sequences
+        [seq0, seq0 + seqs) of a prefill (micro-batch); ``window(0, 0, 0)``
+        restores the whole batch."""
+        if seqs == 0:
+            self.x, self.bt, self.sl = self._x_full, self.kv.block_table, self.kv.seq_lens
+            return
+        self.x = self._x_full[seq0 * seq_len:(seq0 + seqs) * seq_len]
+        self.bt = self.kv.block_table[seq0:seq0 + seqs]
+        self.sl = self.kv.seq_lens[seq0:seq0 + seqs]
 
     # ---- phases of layer li (local index) between the two all-reduces
     def attn_block(self, li: int, n_tok: int, prefill_len: int):
@@ -245,20 +258,20 @@ class RankExecutor:
         kc, vc = self.kv.k[li], self.kv.v[li]
         if self.rope_in_attn and not prefill_len:  # decode: RoPE + KV append inside the attention kernel
             k.linear(lw["wqkv"], self.h, self.qkv, n_tok, self.lin_ws)
-            k.attn_decode_rope_append(self.qkv, kc, vc, self.kv.block_table, self.kv.seq_lens, self.attn, n_tok,
+            k.attn_decode_rope_append(self.qkv, kc, vc, self.bt, self.sl, self.attn, n_tok,
                                       self.hq, self.hkv, self.hd, self.max_ctx, cfg.rope_theta, self.attn_ws)
         elif self.fuse_rope and not prefill_len:  # decode: QKV GEMM with RoPE + KV append in its epilogue
-            k.linear_rope_kv(lw["wqkv"], self.h, self.q, kc, vc, self.kv.block_table, self.kv.seq_lens, n_tok,
+            k.linear_rope_kv(lw["wqkv"], self.h, self.q, kc, vc, self.bt, self.sl, n_tok,
                              prefill_len, self.hq, self.hkv, cfg.rope_theta, self.lin_ws, self.rope_tab)
         else:
             k.linear(lw["wqkv"], self.h, self.qkv, n_tok, self.lin_ws)
-            k.rope_kv_append(self.qkv, self.q, kc, vc, self.kv.block_table, self.kv.seq_lens, n_tok,
+            k.rope_kv_append(self.qkv, self.q, kc, vc, self.bt, self.sl, n_tok,
                              prefill_len, self.hq, self.hkv, self.hd, cfg.rope_theta)
         if prefill_len:
-            k.attn_prefill(self.q, kc, vc, self.kv.block_table, self.kv.seq_lens, self.attn,
+            k.attn_prefill(self.q, kc, vc, self.bt, self.sl, self.attn,
                            n_tok // prefill_len, prefill_len, self.hq, self.hkv, self.hd)
         elif not self.rope_in_attn:
-            k.attn_decode(self.q, kc, vc, self.kv.block_table, self.kv.seq_lens, self.attn, n_tok,
+            k.attn_decode(self.q, kc, vc, self.bt, self.sl, self.attn, n_tok,
                           self.hq, self.hkv, self.hd, self.max_ctx, self.attn_ws)
         # TP=1 decode: the O/down GEMMs leave split tiles as partials and the
         # residual+norm kernel that consumes them does the reduction
@@ -345,7 +358,7 @@ class StageDriver:
                 e.post_block(li, n_tok)
         adv = prefill_len if prefill_len else 1
         for e in self.execs:
-            e.k.advance(e.kv.seq_lens, e.batch, adv)
+            e.k.advance(e.sl, e.sl.numel(), adv)
 
     def head(self, prefill_len: int):
         for e in self.execs:
@@ -489,18 +502,44 @@ class Engine:
                 e.ids_recv = link
 
     # ---------------------------------------------------------------- steps
+    def prefill_microbatches(self, b: int, s: int) -> int:
+        """Micro-batches of the prefill: with more than one stage, stage j+1
+        prefills micro-batch i while stage j runs i+1 (HexGen App. D pipelining;
+        the reference cost model charges the stages' prefill serially,
+        costs.py:240-284). Each micro-batch keeps >= 2048 token rows for the
+        tensor-core GEMMs; HX_PREFILL_MB overrides."""
+        env = os.environ.get("HX_PREFILL_MB")
+        if env:
+            m = max(1, int(env))
+            return m if b % m == 0 else 1
+        if self.num_stages == 1:
+            return 1
+        best = 1
+        for m in range(1, 9):
+            if b % m == 0 and (b // m) * s >= 2048:
+                best = m
+        return best
+
     def _prefill(self, b, s):
-        n = b * s
+        m = self.prefill_microbatches(b, s)
+        mb = b // m
         for d in self.drivers:
             if d.stage == 0:
-                d.embed(n, prefill=True)
-            else:
-                d.recv_hidden(n)
-            d.layers(n, s)
+                d.embed(b * s, prefill=True)
+        for i in range(m):
+            for d in self.drivers:
+                for e in d.execs:
+                    e.window(i * mb, mb, s)
+                if d.stage > 0:
+                    d.recv_hidden(mb * s)
+                d.layers(mb * s, s)
+                if d.stage < self.num_stages - 1:
+                    d.send_hidden(mb * s)
+                for e in d.execs:
+                    e.window(0, 0, 0)
+        for d in self.drivers:
             if d.stage == self.num_stages - 1:
                 d.head(s)
-            else:
-                d.send_hidden(n)
 
     def _decode_compute(self, d: StageDriver, b):
         if d.stage == 0:

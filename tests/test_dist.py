@@ -25,8 +25,8 @@ def _port():
     return p
 
 
-def _run(nproc, args, timeout=600):
-    env = dict(os.environ, OMP_NUM_THREADS="2")
+def _run(nproc, args, timeout=600, **extra_env):
+    env = dict(os.environ, OMP_NUM_THREADS="2", **extra_env)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", f"--master-port={_port()}",
            str(ROOT / "tools" / "dist_generate.py"), *args]
@@ -66,6 +66,17 @@ def test_tp2_stage_nvlink_allreduce(dtype):
 @pytest.mark.skipif(_gpus() < 3, reason="needs >= 3 GPUs")
 def test_nccl_asymmetric_21_fp32_graphs():
     _run(3, ["--plan", "2,1", "--layers", "3,1", "--graphs"])
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(_gpus() < 3, reason="needs >= 3 GPUs")
+def test_nccl_microbatched_prefill_fp32_graphs():
+    """Pipelined prefill (2 micro-batches over NCCL) + P2P decode hand-offs."""
+    _run(3, ["--plan", "2,1", "--layers", "3,1", "--graphs"], HX_PREFILL_MB="2")
+
+
+def test_gloo_microbatched_prefill():
+    _run(2, ["--plan", "1,1", "--layers", "2,2", "--cpu"], HX_PREFILL_MB="2")
 
 
 @pytest.mark.gpu

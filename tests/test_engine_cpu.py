@@ -56,3 +56,16 @@ def test_measured_service_times_has_reference_table_shape():
                                  weights="host", kernels=cpu_kernels)
     assert set(tab) == {(r, t) for r in range(2) for t in set(tasks)}
     assert all(v > 0 for v in tab.values())
+
+
+@pytest.mark.parametrize("tps,layers", [([2, 1], [3, 1]), ([1, 1, 1], [2, 1, 1])])
+def test_microbatched_prefill_matches_golden(tps, layers, monkeypatch):
+    """Pipelined prefill in 2 micro-batches (one sequence each): KV tables,
+    residual rows and hand-offs are windowed per micro-batch; ids unchanged."""
+    monkeypatch.setenv("HX_PREFILL_MB", "2")
+    eng = Engine(simple_plan(tps, layers), TINY, dtype="fp32", batch=2, max_prompt=64, max_out=16,
+                 device="cpu", kernels=cpu_kernels, page_size=16)
+    assert eng.prefill_microbatches(2, 64) == 2
+    r = eng.generate(G["prompt"], 16, return_logits=True)
+    assert np.array_equal(r.ids, G["ids"])
+    assert np.abs(r.logits[..., G["cols"]] - G["col_val"]).max() / G["max_abs"] < 1e-3
