@@ -19,7 +19,7 @@ int launch_decode_mma(int G, int hd, dim3 grid, const void *q, const void *kc, c
                       const int32_t *sl, void *o, int hkv, int page, int maxb, float *ws, int *cnt, cudaStream_t st);
 int launch_decode_tma(int G, dim3 grid, const void *q, const void *kc, const void *vc, const int32_t *bt,
                       const int32_t *sl, void *o, int hkv, int maxb, float *ws, int *cnt, bool rope, float theta,
-                      cudaStream_t st);
+                      cudaStream_t st, int ns);
 static int g_attn_tma = [] {
   const char *e = getenv("HX_ATTN_TMA");
   return e ? atoi(e) : 1;
@@ -344,10 +344,40 @@ static int decode_splits(int batch, int hkv, int max_ctx) {
   // per SM, so splits = floor(2 * 148 / pairs) -- more would add a second,
   // mostly idle wave; each split still streams several 64-key blocks
   const int pairs = batch * hkv;
-  const int target = 2 * 148;
+  static const int target = [] {  // CTAs per wave (2 per SM); HX_ATTN_CTAS overrides (tuning)
+    const char *e = getenv("HX_ATTN_CTAS");
+    return e ? atoi(e) : 2 * 148;
+  }();
   int s = target / pairs;
   const int cap = (max_ctx + 63) / 64;
   s = s < cap ? s : cap;
+  return s < 1 ? 1 : s;
+}
+
+// TMA decode kernel plan. Default: 2 CTAs per SM (4 warps, 3-deep ring), whose
+// ~100 KB of smem lets a CTA become resident next to the preceding QKV GEMM's
+// CTA under PDL and stream its KV pages during the GEMM's tail. HX_ATTN_NS=6:
+// one 8-warp CTA per SM with a 6-deep ring and only as many splits as fill the
+// 148 SMs (fewer splits, shorter combine: faster in isolation at 64-128 (batch,
+// kv-head) pairs, but it cannot overlap the GEMM -- measured slower in the
+// 70B TP=2 decode step, 8.73 vs 8.56 ms per 40 layers).
+static int tma_decode_splits(int batch, int hkv, int max_ctx, int *ns) {
+  const int pairs = batch * hkv;
+  static const int env_ns = [] {
+    const char *e = getenv("HX_ATTN_NS");
+    return e ? atoi(e) : 0;
+  }();
+  const int cap = (max_ctx + 63) / 64;
+  int s, n;
+  if (env_ns == 6) {
+    n = 6;
+    s = 148 / pairs;
+  } else {
+    n = 3;
+    s = decode_splits(batch, hkv, max_ctx);
+  }
+  s = s < cap ? s : cap;
+  *ns = n;
   return s < 1 ? 1 : s;
 }
 
@@ -401,7 +431,9 @@ extern "C" int hx_rope_kv_append(const void *qkv, void *q_out, void *k_cache, vo
 }
 
 extern "C" size_t hx_attn_decode_workspace(int batch, int hq, int hkv, int hd, int max_ctx) {
-  const int s = decode_splits(batch, hkv, max_ctx);
+  int ns;
+  const int s0 = decode_splits(batch, hkv, max_ctx), s1 = tma_decode_splits(batch, hkv, max_ctx, &ns);
+  const int s = s0 > s1 ? s0 : s1;
   if (s <= 1) return 0;
   const size_t counters = kTicketBytes;
   return counters + (size_t)batch * hkv * s * (hq / hkv) * (hd + 2) * sizeof(float);
@@ -414,7 +446,10 @@ extern "C" int hx_attn_decode_paged(const void *q, const void *k_cache, const vo
   if (batch == 0) return 0;
   if (!q || !k_cache || !v_cache || !block_table || !seq_lens || !o || hq % hkv) return HX_ERR_ARG;
   const int G = hq / hkv;
-  const int splits = decode_splits(batch, hkv, max_ctx);
+  const bool tma = dtype == HX_BF16 && hd == 128 && page_size == 64 && g_attn_tma &&
+                   (G == 1 || G == 2 || G == 4 || G == 8 || G == 16);
+  int ns = 3;
+  const int splits = tma ? tma_decode_splits(batch, hkv, max_ctx, &ns) : decode_splits(batch, hkv, max_ctx);
   float *ws = nullptr;
   int *cnt = nullptr;
   if (splits > 1) {
@@ -427,9 +462,9 @@ extern "C" int hx_attn_decode_paged(const void *q, const void *k_cache, const vo
   }
   dim3 grid(batch * hkv, splits);
   const float scale = 1.0f / sqrtf((float)hd);
-  if (dtype == HX_BF16 && hd == 128 && page_size == 64 && g_attn_tma && (G == 1 || G == 2 || G == 4 || G == 8 || G == 16))
+  if (tma)
     return launch_decode_tma(G, grid, q, k_cache, v_cache, block_table, seq_lens, o, hkv, max_blocks, ws, cnt, false,
-                             0.f, as_stream(stream));
+                             0.f, as_stream(stream), ns);
   if (dtype == HX_BF16 && G >= g_attn_mma_min_group && (hd == 64 || hd == 128) && g_attn_mma)  // tensor cores
     return launch_decode_mma(G, hd, grid, q, k_cache, v_cache, block_table, seq_lens, o, hkv, page_size, max_blocks,
                              ws, cnt, as_stream(stream));
@@ -462,7 +497,8 @@ extern "C" int hx_attn_decode_rope_append(const void *qkv, void *k_cache, void *
   if (dtype != HX_BF16 || hd != 128 || page_size != 64 || !g_attn_tma ||
       !(G == 1 || G == 2 || G == 4 || G == 8 || G == 16))
     return HX_ERR_UNSUPPORTED;
-  const int splits = decode_splits(batch, hkv, max_ctx);
+  int ns = 3;
+  const int splits = tma_decode_splits(batch, hkv, max_ctx, &ns);
   float *ws = nullptr;
   int *cnt = nullptr;
   if (splits > 1) {
@@ -473,7 +509,7 @@ extern "C" int hx_attn_decode_rope_append(const void *qkv, void *k_cache, void *
     ws = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(workspace) + kTicketBytes);
   }
   return launch_decode_tma(G, dim3(batch * hkv, splits), qkv, k_cache, v_cache, block_table, seq_lens, o, hkv,
-                           max_blocks, ws, cnt, true, theta, as_stream(stream));
+                           max_blocks, ws, cnt, true, theta, as_stream(stream), ns);
 }
 
 template <typename T, int HD>

@@ -391,8 +391,8 @@ __device__ __forceinline__ uint32_t sw128_addr(uint32_t base, int r, int col) {
   return base + half * 8192 + r * 128 + ((chunk ^ (r & 7)) << 4) + ((col & 7) << 1);
 }
 
-template <int G, bool ROPE>
-__global__ void __launch_bounds__(AM_THREADS)
+template <int G, bool ROPE, int NS, int BPI>
+__global__ void __launch_bounds__(AM_THREADS * BPI)
     attn_decode_tma_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
                            const __nv_bfloat16 *q, const int32_t *bt, const int32_t *seq_lens, __nv_bfloat16 *o,
                            int hkv, int max_blocks, float sl2, float *ws, int *counters, __nv_bfloat16 *kc,
@@ -401,8 +401,8 @@ __global__ void __launch_bounds__(AM_THREADS)
   constexpr uint32_t BLK = PAGE * HD * 2;  // 16 KB per tensor per block
   extern __shared__ __align__(1024) uint8_t smraw[];
   uint8_t *ring = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
-  // ring: [DEC_NS][K 16 KB | V 16 KB]; then Q tile; then barriers
-  __nv_bfloat16 *qs = reinterpret_cast<__nv_bfloat16 *>(ring + DEC_NS * 2 * BLK);
+  // ring: [NS][K 16 KB | V 16 KB]; then Q tile; then barriers
+  __nv_bfloat16 *qs = reinterpret_cast<__nv_bfloat16 *>(ring + NS * 2 * BLK);
   uint64_t *full = reinterpret_cast<uint64_t *>(qs + 16 * LD);
   float *red = reinterpret_cast<float *>(ring);  // [4 warps][16][HD + 2], reuses the ring at the end
   __shared__ int s_last;
@@ -427,7 +427,7 @@ __global__ void __launch_bounds__(AM_THREADS)
   const int safe = min(nblk, max(0, pos / PAGE - t0 / PAGE));  // blocks not holding the new token
   const uint64_t pol = l2_policy_evict_first();  // each K/V byte is read once per step
   auto issue = [&](int i) {
-    const int s = i % DEC_NS;
+    const int s = i % NS;
     const int row = (btb[t0 / PAGE + i] * hkv + kvh) * PAGE;
     uint8_t *kd = ring + s * 2 * BLK, *vd = kd + BLK;
     mbar_arrive_expect_tx(&full[s], 2 * BLK);
@@ -436,11 +436,11 @@ __global__ void __launch_bounds__(AM_THREADS)
     tma_load_2d(vd, &tmv, &full[s], 0, row, pol);
     tma_load_2d(vd + BLK / 2, &tmv, &full[s], 64, row, pol);
   };
-  const int pre = min(DEC_NS - 1, safe);
+  const int pre = min(NS, safe);
   if (threadIdx.x == 0) {
     tma_prefetch(&tmk);
     tma_prefetch(&tmv);
-    for (int s = 0; s < DEC_NS; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
     fence_barrier_init();
     for (int i = 0; i < pre; ++i) issue(i);
   }
@@ -454,7 +454,7 @@ __global__ void __launch_bounds__(AM_THREADS)
     const float inv_freq = 1.0f / powf(theta, (float)(2 * i) / 128.0f);
     float sn, cs;
     sincosf((float)pos * inv_freq, &sn, &cs);
-    for (int r = threadIdx.x >> 6; r < 16; r += AM_THREADS / 64) {
+    for (int r = threadIdx.x >> 6; r < 16; r += AM_THREADS * BPI / 64) {
       float y1 = 0.f, y2 = 0.f;
       if (r < G) {
         const float x1 = to_f32(row[(kvh * G + r) * HD + i]), x2 = to_f32(row[(kvh * G + r) * HD + i + 64]);
@@ -479,7 +479,7 @@ __global__ void __launch_bounds__(AM_THREADS)
       fence_proxy_async_global();  // the page is about to be read back by TMA
     }
   } else {
-    for (int i = threadIdx.x; i < 16 * (HD / 8); i += AM_THREADS) {
+    for (int i = threadIdx.x; i < 16 * (HD / 8); i += AM_THREADS * BPI) {
       const int r = i / (HD / 8), c = (i % (HD / 8)) * 8;
       uint4 v = make_uint4(0, 0, 0, 0);
       if (r < G) v = *reinterpret_cast<const uint4 *>(q + ((size_t)b * hq + kvh * G + r) * HD + c);
@@ -487,8 +487,9 @@ __global__ void __launch_bounds__(AM_THREADS)
     }
   }
   __syncthreads();
+  int issued = pre;  // meaningful in thread 0 only
   if (threadIdx.x == 0)
-    for (int i = pre; i < DEC_NS - 1 && i < nblk; ++i) issue(i);
+    for (; issued < NS && issued < nblk; ++issued) issue(issued);
   uint32_t qf[HD / 16][4];
 #pragma unroll
   for (int c = 0; c < HD / 16; ++c) {
@@ -502,14 +503,18 @@ __global__ void __launch_bounds__(AM_THREADS)
 #pragma unroll
     for (int e = 0; e < 4; ++e) oacc[n][e] = 0.f;
   float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
-  for (int kb = 0; kb < nblk; ++kb) {
-    if (kb > 0) __syncthreads();  // every warp is done with block kb - 1's stage
-    if (threadIdx.x == 0 && kb + DEC_NS - 1 < nblk) issue(kb + DEC_NS - 1);
-    const int s = kb % DEC_NS;
-    mbar_wait(&full[s], (kb / DEC_NS) & 1);
+  // BPI blocks per iteration: warp w takes 16 keys of block kb0 + w / 4
+  const int wb = warp >> 2, wk = warp & 3;
+  for (int kb0 = 0; kb0 < nblk; kb0 += BPI) {
+    if (kb0 > 0) __syncthreads();  // every warp is done with the previous iteration's stages
+    if (threadIdx.x == 0)
+      for (; issued < nblk && issued < kb0 + NS; ++issued) issue(issued);
+    const int kb = kb0 + wb;
+    const int s = kb % NS;
+    const int k0 = t0 + kb * PAGE + 16 * wk;  // this warp's 16 keys
+    if (kb < nblk) mbar_wait(&full[s], (kb / NS) & 1);
     const uint32_t kbase = smem_u32(ring + s * 2 * BLK), vbase = kbase + BLK;
-    const int k0 = t0 + kb * PAGE + 16 * warp;  // this warp's 16 keys
-    if (k0 < t1) {
+    if (kb < nblk && k0 < t1) {
       float sc[2][4];
 #pragma unroll
       for (int j = 0; j < 2; ++j)
@@ -517,7 +522,7 @@ __global__ void __launch_bounds__(AM_THREADS)
         for (int e = 0; e < 4; ++e) sc[j][e] = 0.f;
 #pragma unroll
       for (int c = 0; c < HD / 16; ++c) {
-        const int row = 16 * warp + (lane & 7) + 8 * (lane >> 4);
+        const int row = 16 * wk + (lane & 7) + 8 * (lane >> 4);
         const int col = 16 * c + 8 * ((lane >> 3) & 1);
         uint32_t b0, b1, b2, b3;
         ldsm_x4(sw128_addr(kbase, row, col), b0, b1, b2, b3);
@@ -537,7 +542,7 @@ __global__ void __launch_bounds__(AM_THREADS)
       a[3] = pack_bf16(sc[1][2], sc[1][3]);
 #pragma unroll
       for (int n = 0; n < HD / 8; n += 2) {
-        const int row = 16 * warp + (lane & 7) + 8 * ((lane >> 3) & 1);
+        const int row = 16 * wk + (lane & 7) + 8 * ((lane >> 3) & 1);
         const int col = 8 * n + 8 * (lane >> 4);
         uint32_t b0, b1, b2, b3;
         ldsm_x4_t(sw128_addr(vbase, row, col), b0, b1, b2, b3);
@@ -568,15 +573,15 @@ __global__ void __launch_bounds__(AM_THREADS)
   }
   __syncthreads();
   const size_t pair = (size_t)b * hkv + kvh;
-  for (int w = threadIdx.x; w < G * HD; w += AM_THREADS) {
+  for (int w = threadIdx.x; w < G * HD; w += AM_THREADS * BPI) {
     const int r = w / HD, d = w % HD;
     float M = -INFINITY;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) M = fmaxf(M, red[(i * 16 + r) * (HD + 2) + HD]);
+    for (int i = 0; i < 4 * BPI; ++i) M = fmaxf(M, red[(i * 16 + r) * (HD + 2) + HD]);
     float L = 0.f, A = 0.f;
     if (M != -INFINITY) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < 4 * BPI; ++i) {
         const float c = exp2f(red[(i * 16 + r) * (HD + 2) + HD] - M);
         L += red[(i * 16 + r) * (HD + 2) + HD + 1] * c;
         A += red[(i * 16 + r) * (HD + 2) + d] * c;
@@ -599,35 +604,62 @@ __global__ void __launch_bounds__(AM_THREADS)
   }
   __syncthreads();
   if (!s_last) return;
-  for (int w = threadIdx.x; w < G * HD; w += AM_THREADS) {
-    const int r = w / HD, d = w % HD;
+  // combine the splits: all (m, l) pairs into smem first, then one scale per
+  // (row, split), then the rows with every split's loads independent (the
+  // split-combine tail is latency-bound: no load may wait on another)
+  float *ml = red;                       // [splits][G] x (m -> scale, l)
+  float *lsum = red + 2 * G * splits;    // [G]
+  const float *wsp = ws + pair * splits * G * (HD + 2);
+  for (int i = threadIdx.x; i < G * splits; i += AM_THREADS * BPI) {
+    const float2 v = __ldcg(reinterpret_cast<const float2 *>(wsp + (size_t)i * (HD + 2) + HD));
+    ml[2 * i] = v.x;
+    ml[2 * i + 1] = v.y;
+  }
+  __syncthreads();
+  if (threadIdx.x < G) {
+    const int r = threadIdx.x;
     float M = -INFINITY;
-    for (int s2 = 0; s2 < splits; ++s2) M = fmaxf(M, __ldcg(ws + ((pair * splits + s2) * G + r) * (HD + 2) + HD));
-    float L = 0.f, A = 0.f;
+    for (int s2 = 0; s2 < splits; ++s2) M = fmaxf(M, ml[2 * (s2 * G + r)]);
+    float L = 0.f;
     for (int s2 = 0; s2 < splits; ++s2) {
-      const float *part = ws + ((pair * splits + s2) * G + r) * (HD + 2);
-      const float ms = __ldcg(part + HD);
-      if (ms == -INFINITY) continue;
-      const float c = exp2f(ms - M);
-      L += __ldcg(part + HD + 1) * c;
-      A += __ldcg(part + d) * c;
+      const float ms = ml[2 * (s2 * G + r)];
+      const float c = ms == -INFINITY ? 0.f : exp2f(ms - M);
+      L += ml[2 * (s2 * G + r) + 1] * c;
+      ml[2 * (s2 * G + r)] = c;
     }
-    o[((size_t)b * hq + kvh * G + r) * HD + d] = __float2bfloat16_rn(A / L);
+    lsum[r] = L;
+  }
+  __syncthreads();
+#pragma unroll 4
+  for (int w = threadIdx.x; w < G * HD / 2; w += AM_THREADS * BPI) {
+    const int r = w / (HD / 2), d = (w % (HD / 2)) * 2;
+    float2 A = make_float2(0.f, 0.f);
+    for (int s2 = 0; s2 < splits; ++s2) {
+      const float c = ml[2 * (s2 * G + r)];
+      if (c == 0.f) continue;
+      const float2 p = __ldcg(reinterpret_cast<const float2 *>(wsp + (size_t)(s2 * G + r) * (HD + 2) + d));
+      A.x += p.x * c;
+      A.y += p.y * c;
+    }
+    const float L = lsum[r];
+    __nv_bfloat16 *dst = o + ((size_t)b * hq + kvh * G + r) * HD + d;
+    dst[0] = __float2bfloat16_rn(A.x / L);
+    dst[1] = __float2bfloat16_rn(A.y / L);
   }
 }
 
-template <int G, bool ROPE>
+template <int G, bool ROPE, int NS, int BPI>
 static int launch_decode_tma_g(dim3 grid, const CUtensorMap &mk, const CUtensorMap &mv, const void *q,
                                const int32_t *bt, const int32_t *sl, void *o, int hkv, int maxb, float *ws, int *cnt,
                                void *kc, void *vc, float theta, cudaStream_t st) {
-  const size_t smem = 1024 + DEC_NS * 2 * 16384 + 16 * 136 * 2 + DEC_NS * 8 + 16;
+  const size_t smem = 1024 + NS * 2 * 16384 + 16 * 136 * 2 + NS * 8 + 16;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(attn_decode_tma_kernel<G, ROPE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(attn_decode_tma_kernel<G, ROPE, NS, BPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
   const float sl2 = 1.4426950408889634f / sqrtf(128.f);
-  return launch(attn_decode_tma_kernel<G, ROPE>, grid, dim3(AM_THREADS), smem, st, mk, mv, (const __nv_bfloat16 *)q,
+  return launch(attn_decode_tma_kernel<G, ROPE, NS, BPI>, grid, dim3(AM_THREADS * BPI), smem, st, mk, mv, (const __nv_bfloat16 *)q,
                 bt, sl, (__nv_bfloat16 *)o, hkv, maxb, sl2, ws, cnt, (__nv_bfloat16 *)kc, (__nv_bfloat16 *)vc, theta);
 }
 
@@ -635,7 +667,7 @@ static int launch_decode_tma_g(dim3 grid, const CUtensorMap &mk, const CUtensorM
 // new token's k (rotated) and v are appended by the kernel itself.
 int launch_decode_tma(int G, dim3 grid, const void *q, const void *kc, const void *vc, const int32_t *bt,
                       const int32_t *sl, void *o, int hkv, int maxb, float *ws, int *cnt, bool rope, float theta,
-                      cudaStream_t st) {
+                      cudaStream_t st, int ns) {
   CUtensorMap mk, mv;
   // the pool size is not part of the C-ABI: declare 2^28 rows (64 GB of K); only
   // rows of blocks named by the block table are ever addressed
@@ -644,9 +676,12 @@ int launch_decode_tma(int G, dim3 grid, const void *q, const void *kc, const voi
   if (!rc) rc = make_tma_bf16_sw128(&mv, vc, rows, 128, 128, 64);
   if (rc) return rc;
   void *k = const_cast<void *>(kc), *v = const_cast<void *>(vc);
-#define HX_TMA_G(GG)                                                                                             \
-  return rope ? launch_decode_tma_g<GG, true>(grid, mk, mv, q, bt, sl, o, hkv, maxb, ws, cnt, k, v, theta, st) \
-              : launch_decode_tma_g<GG, false>(grid, mk, mv, q, bt, sl, o, hkv, maxb, ws, cnt, k, v, theta, st)
+#define HX_TMA_G(GG)                                                                                               \
+  if (ns == 6)                                                                                                     \
+    return rope ? launch_decode_tma_g<GG, true, 6, 2>(grid, mk, mv, q, bt, sl, o, hkv, maxb, ws, cnt, k, v, theta, st) \
+                : launch_decode_tma_g<GG, false, 6, 2>(grid, mk, mv, q, bt, sl, o, hkv, maxb, ws, cnt, k, v, theta, st); \
+  return rope ? launch_decode_tma_g<GG, true, 3, 1>(grid, mk, mv, q, bt, sl, o, hkv, maxb, ws, cnt, k, v, theta, st)   \
+              : launch_decode_tma_g<GG, false, 3, 1>(grid, mk, mv, q, bt, sl, o, hkv, maxb, ws, cnt, k, v, theta, st)
   switch (G) {
     case 1: HX_TMA_G(1);
     case 2: HX_TMA_G(2);
