@@ -83,7 +83,11 @@ int hx_residual_add_rmsnorm(float *x, const float *delta, const float *gain,
  * Under PDL the kernel streams its first weight tiles before waiting on the
  * previous kernel: W must not be written by the kernel launched just before
  * it on the stream (weights are static; hx_pack_weight never triggers early). */
-enum hx_linear_flags { HX_LINEAR_ACCUMULATE = 1, HX_LINEAR_PACKED = 2, HX_LINEAR_DEFER_REDUCE = 4 };
+enum hx_linear_flags { HX_LINEAR_ACCUMULATE = 1, HX_LINEAR_PACKED = 2, HX_LINEAR_DEFER_REDUCE = 4,
+                       HX_LINEAR_L2_PREFETCH = 8 };
+/* HX_LINEAR_L2_PREFETCH (decode shapes): before its PDL wait each CTA also
+ * prefetches its next weight tiles (HX_GEMM_L2PF, default 16) into L2 -- for a
+ * GEMM that follows a latency-bound kernel (the TP all-reduce). */
 /* HX_LINEAR_DEFER_REDUCE (decode shapes, fp32 Y): tiles split across CTAs are
  * left as fp32 partial slots in the workspace instead of being reduced by a
  * ticketed last CTA; the next kernel on the stream must be

@@ -363,6 +363,7 @@ struct SKArgs {
   float *ws;
   int *counters;
   unsigned long long *trace;  // optional per-CTA timeline (hx_debug_trace): start, wait done, end, smid
+  int l2pf;                   // weight tiles beyond the smem ring prefetched into L2 before the PDL wait
   EpiArgs epi;
 };
 
@@ -526,6 +527,14 @@ __global__ void __launch_bounds__(192, 2)
       for (int i = 0; i < pre; ++i) {  // weights first: they do not depend on the previous kernel
         mbar_arrive_expect_tx(&full[i], A_BYTES + B_BYTES);
         load_w(i, u0 + i);
+      }
+      // ...and the next l2pf tiles into L2, so HBM keeps streaming this GEMM's
+      // weights while the previous kernel (all-reduce, norm, attention tail)
+      // is latency-bound; after the wait those tiles arrive at L2 speed
+      for (int i = pre; i < min(n, pre + p.l2pf); ++i) {
+        const int u = u0 + i;
+        if (p.w_packed) tma_prefetch_l2_2d(&tm_w, 0, u * BM);
+        else tma_prefetch_l2_2d(&tm_w, (u % p.KB) * BK, (u / p.KB) * BM);
       }
       pdl_wait();
       if (p.trace) p.trace[8 * c + 1] = globaltimer();
@@ -1107,6 +1116,11 @@ static int linear_impl(const void *w, const void *x, void *y, int dtype, int y_d
     if (rc) return rc;
     if ((rc = make_map(&mb, x, n_tok, k_dim, k_dim, pl.bn))) return rc;
     SKArgs sk{};
+    static const int l2pf = [] {
+      const char *e = getenv("HX_GEMM_L2PF");
+      return e ? atoi(e) : 16;
+    }();
+    sk.l2pf = (flags & HX_LINEAR_L2_PREFETCH) ? l2pf : 0;
     sk.c = y; sk.ldm = 1; sk.ldn = ldy; sk.M = n_out; sk.N = n_tok;
     sk.c_bf16 = p.c_bf16; sk.accumulate = accumulate; sk.w_packed = packed; sk.epi = epi;
     sk.defer = (flags & HX_LINEAR_DEFER_REDUCE) ? 1 : 0;

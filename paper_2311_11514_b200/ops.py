@@ -182,11 +182,16 @@ def splitk_residual_rmsnorm(x, y, workspace, n_tok, k_dim, gain, out, eps):
                                              eps, _stream()), "hx_splitk_residual_rmsnorm")
 
 
-def linear(w, x, y, n_tok, workspace=None, accumulate=False, defer_reduce=False):
+HX_LINEAR_L2_PREFETCH = 8
+
+
+def linear(w, x, y, n_tok, workspace=None, accumulate=False, defer_reduce=False, l2_prefetch=False):
     """y[:n_tok, :n_out] (+)= x[:n_tok] @ w.T ; w [n_out, K] row-major tensor
-    or a PackedWeight. defer_reduce: see splitk_residual_rmsnorm."""
+    or a PackedWeight. defer_reduce: see splitk_residual_rmsnorm. l2_prefetch:
+    stream more weight tiles into L2 before the PDL wait (after an all-reduce)."""
     n_out, k = w.shape
-    flags = (HX_LINEAR_ACCUMULATE if accumulate else 0) | (HX_LINEAR_DEFER_REDUCE if defer_reduce else 0)
+    flags = (HX_LINEAR_ACCUMULATE if accumulate else 0) | (HX_LINEAR_DEFER_REDUCE if defer_reduce else 0) | \
+        (HX_LINEAR_L2_PREFETCH if l2_prefetch else 0)
     if isinstance(w, PackedWeight):
         flags |= HX_LINEAR_PACKED
         wp = w.data
