@@ -277,8 +277,19 @@ def gemm_roofline(eng, cfg, w, hbm, reps=5):
         ts = s0.elapsed_time(s1) / 1e3 / reps
         per_shape[name] = {"shape": list(sub[0][0].shape), "us_per_launch": round(ts / len(sub) * 1e6, 2),
                            "GBps": round(gb / ts / 1e9, 1)}
+    traffic = None
+    tfile = ROOT / "profiles" / "r01" / "gemm_traffic_7b.json"
+    if cfg.name == "llama2-7b" and w["batch"] == 8 and tfile.exists():
+        # dram read+write per launch from one ncu --set full capture of the same
+        # kernel on this workload (one layer's qkv/o/gate_up/down), for comparison
+        # with the algorithmic bytes per launch
+        t = json.loads(tfile.read_text())
+        traffic = {"bytes_per_launch": round(t["traffic_bytes_per_launch_avg"]),
+                   "algorithmic_bytes_per_launch": round(t["algorithmic_bytes_per_launch_avg"]),
+                   "ratio": round(t["traffic_bytes_per_launch_avg"] / t["algorithmic_bytes_per_launch_avg"], 4),
+                   "source": "profiles/r01/gemm_traffic_7b.json"}
     return {"bound": "hbm", "kernel": "hx_linear (tcgen05 stream-K decode GEMM)", "achieved": round(achieved, 1),
-            "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": None,
+            "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": traffic,
             "launches_per_step": len(seq), "avg_launch_us": round(t / len(seq) * 1e6, 2),
             "bytes_per_step": nbytes, "gemm_ms_per_step": round(t * 1e3, 4), "per_shape": per_shape}
 

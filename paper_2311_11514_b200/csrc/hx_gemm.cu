@@ -1157,7 +1157,17 @@ static int linear_impl(const void *w, const void *x, void *y, int dtype, int y_d
           default: return launch_sk<16, 6>(ma, mb, sk, st);
         }
       }
-      case 32: return launch_sk<32, 5>(ma, mb, sk, st);
+      case 32: {
+        static const int stages = [] {
+          const char *e = getenv("HX_SK32_STAGES");
+          return e ? atoi(e) : 5;
+        }();
+        switch (stages) {
+          case 7: return launch_sk<32, 7>(ma, mb, sk, st);
+          case 9: return launch_sk<32, 9>(ma, mb, sk, st);
+          default: return launch_sk<32, 5>(ma, mb, sk, st);
+        }
+      }
       default: return launch_sk<64, 4>(ma, mb, sk, st);
     }
   } else {
