@@ -99,3 +99,15 @@ def test_peer_allreduce_push_equals_pull(n):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count("push==pull: True, replicated: True") == n, r.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("plan,layers", [("1,2", "2,2"), ("2,2", "3,1"), ("1,2,1", "1,2,1")])
+def test_nccl_reshard_topologies_fp32_graphs(plan, layers):
+    """TP_j -> TP_{j+1} reshards of the [4,2,2] shape class (fan-out 1 -> 2,
+    equal 2 -> 2, fan-in 2 -> 1, token return to a wider stage 0) over the
+    P2P hand-off kernels inside the decode graphs; ids must match the oracle."""
+    n = sum(int(x) for x in plan.split(","))
+    if _gpus() < n:
+        pytest.skip(f"needs {n} GPUs")
+    _run(n, ["--plan", plan, "--layers", layers, "--graphs"])
