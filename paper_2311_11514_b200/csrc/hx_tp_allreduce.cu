@@ -121,15 +121,20 @@ __global__ void __launch_bounds__(1024)
 // data itself is there: an inbox element holds the sentinel -0.0f (0x80000000)
 // until a peer's store lands (pushed values are sanitised -0.0 -> +0.0, which
 // cannot change any sum). One one-way NVLink trip per call, no fences.
-// Inbox per rank: [3 buffers][tp senders][max_tok][hidden] fp32; call k uses
-// buffer k % 3 and re-arms buffer (k + 2) % 3 (consumed at call k - 1; no peer
-// can write it again before call k + 2, which needs this rank's call k + 1
-// data). The call counter lives in state[0] and is bumped by the last CTA.
+// Inbox per rank: [2 buffers][tp senders][max_tok][hidden] fp32; call k uses
+// buffer k & 1 and every element is re-armed in place right after it is read
+// (a peer writes buffer k & 1 again only at call k + 2, which needs this
+// rank's call k + 1 data, pushed after this kernel has completed).
+// One token row = a cluster of AR_CL CTAs, each owning hidden / AR_CL features,
+// so the push/poll traffic spreads over 4x the SMs; the RMS sum of squares is
+// combined across the cluster through DSMEM. The call counter lives in
+// state[0] and is bumped by the grid's last CTA.
 struct ArInbox {
   float *box[kMaxTP];  // rank r's inbox (peer-mapped; own = local)
 };
 
 constexpr uint32_t kSentinel = 0x80000000u;
+constexpr int AR_CL = 4;
 
 __device__ __forceinline__ uint4 ld_volatile_u4(const void *p) {
   uint4 v;
@@ -146,57 +151,59 @@ __device__ __forceinline__ float4 sanitize(float4 v) {  // -0.0 -> +0.0 (bitwise
 }
 
 template <typename TO>
-__global__ void __launch_bounds__(1024)
-    tp_ar_push_rmsnorm_kernel(float *x, const float *own, ArInbox ib, int rank, int tp, int max_tok, int n_tok,
-                              int *state, const float *gain, TO *out, int hidden, float eps) {
+__global__ void __launch_bounds__(256)
+    tp_ar_push_rmsnorm_kernel(float *x, const float *own, ArInbox ib, int rank, int tp, int max_tok, int *state,
+                              const float *gain, TO *out, int hidden, float eps) {
   pdl_trigger();
-  pdl_wait();  // this rank's partial (previous kernel) is complete
-  __shared__ float red[32];
-  const int t = blockIdx.x;
-  const int call = *(volatile int *)state;
-  const int buf = call % 3, rearm = (call + 2) % 3;
+  __shared__ float red[8];
+  __shared__ float part;
+  const unsigned cr = cluster_rank();
+  const int t = blockIdx.x / AR_CL;
+  const int per = hidden / AR_CL, base = (int)cr * per;
   const size_t row = (size_t)hidden;
+  constexpr int MAXV = 2;  // hidden <= AR_CL * 2 * 4 * 256 = 8192
+  float4 gv[MAXV];
+#pragma unroll
+  for (int i = 0; i < MAXV; ++i) {  // the gain is a weight: fetch it before the wait
+    const int n = base + (i * 256 + threadIdx.x) * 4;
+    if (out && n < base + per) gv[i] = __ldg(reinterpret_cast<const float4 *>(gain + n));
+  }
+  pdl_wait();  // this rank's partial (previous kernel) is complete
+  const int call = *(volatile int *)state;
+  const int buf = call & 1;
   float *mine = ib.box[rank];
-  constexpr int MAXV = 2;  // hidden <= 8192
   float4 p[MAXV];
-  // 1. push my partial row t to every peer (remote stores; nothing waits on them here)
+  // 1. push my partial slice of row t to every peer (remote stores, fire and forget)
 #pragma unroll
   for (int i = 0; i < MAXV; ++i) {
-    const int n = (i * 1024 + threadIdx.x) * 4;
-    if (n >= hidden) continue;
+    const int n = base + (i * 256 + threadIdx.x) * 4;
+    if (n >= base + per) continue;
     p[i] = sanitize(__ldcs(reinterpret_cast<const float4 *>(own + (size_t)t * row + n)));
     for (int r = 0; r < tp; ++r)
       if (r != rank)
         *reinterpret_cast<float4 *>(ib.box[r] + (((size_t)buf * tp + rank) * max_tok + t) * row + n) = p[i];
   }
-  // 2. re-arm the buffer consumed by the previous call (all rows this CTA owns)
+  // 2. poll my inbox for every peer's slice, re-arm it in place, sum in rank order
+  //    (bitwise identical on all ranks), residual
   const float4 s4 = make_float4(__uint_as_float(kSentinel), __uint_as_float(kSentinel), __uint_as_float(kSentinel),
                                 __uint_as_float(kSentinel));
-  for (int rr = t; rr < max_tok; rr += n_tok)
-#pragma unroll
-    for (int i = 0; i < MAXV; ++i) {
-      const int n = (i * 1024 + threadIdx.x) * 4;
-      if (n >= hidden) continue;
-      for (int r = 0; r < tp; ++r)
-        if (r != rank) *reinterpret_cast<float4 *>(mine + (((size_t)rearm * tp + r) * max_tok + rr) * row + n) = s4;
-    }
-  // 3. poll my inbox for every peer's row t, sum in rank order (bitwise identical on all ranks)
   float ss = 0.f;
   float4 v[MAXV];
 #pragma unroll
   for (int i = 0; i < MAXV; ++i) {
-    const int n = (i * 1024 + threadIdx.x) * 4;
-    if (n >= hidden) continue;
+    const int n = base + (i * 256 + threadIdx.x) * 4;
+    if (n >= base + per) continue;
     float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int r = 0; r < tp; ++r) {
       float4 q = p[i];
       if (r != rank) {
-        const float *src = mine + (((size_t)buf * tp + r) * max_tok + t) * row + n;
+        float *src = mine + (((size_t)buf * tp + r) * max_tok + t) * row + n;
         uint4 u = ld_volatile_u4(src);
         for (uint32_t spins = 0; has_sentinel(u); ++spins) {
           if (spins > (1u << 26)) __trap();  // a peer never arrived: fail loudly, never hang
           u = ld_volatile_u4(src);
         }
+        *reinterpret_cast<float4 *>(src) = s4;
         q = make_float4(__uint_as_float(u.x), __uint_as_float(u.y), __uint_as_float(u.z), __uint_as_float(u.w));
       }
       sum.x += q.x; sum.y += q.y; sum.z += q.z; sum.w += q.w;
@@ -207,23 +214,28 @@ __global__ void __launch_bounds__(1024)
     v[i] = acc;
     ss += acc.x * acc.x + acc.y * acc.y + acc.z * acc.z + acc.w * acc.w;
   }
+  // 3. RMSNorm across the cluster (DSMEM), same summation order in every CTA
   if (out) {
     ss = warp_sum(ss);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
     __syncthreads();
+    if (threadIdx.x == 0) {
+      float s2 = 0.f;
+      for (int i = 0; i < 8; ++i) s2 += red[i];
+      part = s2;
+    }
+    cluster_sync_all();
     float tot = 0.f;
-    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) tot += red[i];
+    for (int c = 0; c < AR_CL; ++c) tot += dsmem_ld_f32(&part, c);
+    cluster_sync_all();  // peers have read `part` before this CTA may exit
     const float inv = 1.0f / sqrtf(tot / (float)hidden + eps);
+    TO *o = out + (size_t)t * row;
 #pragma unroll
     for (int i = 0; i < MAXV; ++i) {
-      const int n = (i * 1024 + threadIdx.x) * 4;
-      if (n >= hidden) continue;
-      const float4 g = *reinterpret_cast<const float4 *>(gain + n);
-      TO *o = out + (size_t)t * row + n;
-      o[0] = from_f32<TO>((v[i].x * inv) * g.x);
-      o[1] = from_f32<TO>((v[i].y * inv) * g.y);
-      o[2] = from_f32<TO>((v[i].z * inv) * g.z);
-      o[3] = from_f32<TO>((v[i].w * inv) * g.w);
+      const int n = base + (i * 256 + threadIdx.x) * 4;
+      if (n >= base + per) continue;
+      const float4 g = gv[i];
+      store4(o + n, (v[i].x * inv) * g.x, (v[i].y * inv) * g.y, (v[i].z * inv) * g.z, (v[i].w * inv) * g.w);
     }
   }
   __syncthreads();
@@ -295,7 +307,7 @@ extern "C" int hx_tp_allreduce_residual_rmsnorm(float *x, const float *const *pa
 }
 
 extern "C" size_t hx_tp_inbox_bytes(int tp, int max_tok, int hidden) {
-  return (size_t)3 * tp * max_tok * hidden * sizeof(float);
+  return (size_t)2 * tp * max_tok * hidden * sizeof(float);
 }
 
 extern "C" int hx_tp_inbox_init(void *inbox, int tp, int max_tok, int hidden, hx_stream_t stream) {
@@ -311,14 +323,15 @@ extern "C" int hx_tp_allreduce_push_residual_rmsnorm(float *x, const float *own_
                                                      hx_stream_t stream) {
   if (n_tok == 0) return 0;
   if (!x || !own_part || !inboxes || !state || tp < 1 || tp > kMaxTP || rank < 0 || rank >= tp ||
-      n_tok > max_tok || hidden % 4 || hidden > 8192 || (out && !gain))
+      n_tok > max_tok || hidden % (4 * AR_CL) || hidden > 8192 || (out && !gain))
     return HX_ERR_ARG;
   ArInbox ib{};
   for (int r = 0; r < tp; ++r) ib.box[r] = inboxes[r];
   cudaStream_t st = as_stream(stream);
+  const dim3 grid(n_tok * AR_CL);
   if (out_dtype == HX_BF16)
-    return launch(tp_ar_push_rmsnorm_kernel<__nv_bfloat16>, dim3(n_tok), dim3(1024), 0, st, x, own_part, ib, rank,
-                  tp, max_tok, n_tok, state, gain, (__nv_bfloat16 *)out, hidden, eps);
-  return launch(tp_ar_push_rmsnorm_kernel<float>, dim3(n_tok), dim3(1024), 0, st, x, own_part, ib, rank, tp,
-                max_tok, n_tok, state, gain, (float *)out, hidden, eps);
+    return launch_cluster(tp_ar_push_rmsnorm_kernel<__nv_bfloat16>, grid, dim3(256), 0, st, AR_CL, x, own_part, ib,
+                          rank, tp, max_tok, state, gain, (__nv_bfloat16 *)out, hidden, eps);
+  return launch_cluster(tp_ar_push_rmsnorm_kernel<float>, grid, dim3(256), 0, st, AR_CL, x, own_part, ib, rank, tp,
+                        max_tok, state, gain, (float *)out, hidden, eps);
 }

@@ -60,10 +60,17 @@ def main():
                 outs.append(out.clone())
             torch.cuda.synchronize()
             res[mode] = (x.clone(), torch.stack(outs))
-        same = torch.equal(res["pull"][0], res["push"][0]) and torch.equal(res["pull"][1], res["push"][1])
+        # the all-reduced residual must be bitwise identical; the normalised bf16
+        # output may differ by 1 ulp (the push kernel reduces the RMS over a
+        # 4-CTA cluster, the pull kernel over one 1024-thread CTA)
+        d = (res["pull"][1].float() - res["push"][1].float()).abs()
+        ulp = res["pull"][1].float().abs().clamp_min(1e-30) * 2.0 ** -7
+        same = torch.equal(res["pull"][0], res["push"][0]) and bool((d <= ulp).all())
         xs = [torch.empty_like(res["push"][0]) for _ in range(tp)]
         dist.all_gather(xs, res["push"][0])
-        repl = all(torch.equal(xs[0], t) for t in xs)
+        os_ = [torch.empty_like(res["push"][1]) for _ in range(tp)]
+        dist.all_gather(os_, res["push"][1])
+        repl = all(torch.equal(xs[0], t) for t in xs) and all(torch.equal(os_[0], t) for t in os_)
         print(f"rank {rank} check push==pull: {same}, replicated: {repl}", flush=True)
         dist.barrier()
         os._exit(0 if same and repl else 1)
