@@ -283,10 +283,10 @@ def gemm_roofline(eng, cfg, w, hbm, reps=5):
         # dram read+write per launch from one ncu --set full capture of the same
         # kernel on this workload (one layer's qkv/o/gate_up/down), for comparison
         # with the algorithmic bytes per launch
-        t = json.loads(tfile.read_text())
-        traffic = {"bytes_per_launch": round(t["traffic_bytes_per_launch_avg"]),
-                   "algorithmic_bytes_per_launch": round(t["algorithmic_bytes_per_launch_avg"]),
-                   "ratio": round(t["traffic_bytes_per_launch_avg"] / t["algorithmic_bytes_per_launch_avg"], 4),
+        tj = json.loads(tfile.read_text())
+        traffic = {"bytes_per_launch": round(tj["traffic_bytes_per_launch_avg"]),
+                   "algorithmic_bytes_per_launch": round(tj["algorithmic_bytes_per_launch_avg"]),
+                   "ratio": round(tj["traffic_bytes_per_launch_avg"] / tj["algorithmic_bytes_per_launch_avg"], 4),
                    "source": "profiles/r01/gemm_traffic_7b.json"}
     return {"bound": "hbm", "kernel": "hx_linear (tcgen05 stream-K decode GEMM)", "achieved": round(achieved, 1),
             "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": traffic,

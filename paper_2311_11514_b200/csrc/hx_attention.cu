@@ -41,38 +41,56 @@ __device__ __forceinline__ size_t page_index(const int32_t *bt, int b, int pos, 
 }
 
 // ------------------------------------------------------------- RoPE + append
-// grid (token, head of the packed q|k|v row); hd/2 threads, one rotate-half
-// pair each (v heads: plain copy into the page).
-template <typename T>
-__global__ void rope_append_kernel(const T *qkv, T *q_out, T *kc, T *vc, const int32_t *bt,
-                                   const int32_t *seq_lens, int prefill_len, int hq, int hkv, int hd,
-                                   int page, int max_blocks, float theta) {
+// One CTA per token: the (cos, sin) of the token's position are computed once
+// into smem (the same fp32 arithmetic per pair index as everywhere else) and
+// shared by all q / k heads; threads then sweep (head, 4 rotate-half pairs)
+// tasks with 4-element vector loads and stores (v heads: plain copy into the
+// page). The old (token, head) grid launched 96 tiny CTAs per token with
+// scalar accesses and recomputed the transcendental per head.
+template <typename T, int VEC>
+__global__ void __launch_bounds__(256)
+    rope_append_kernel(const T *qkv, T *q_out, T *kc, T *vc, const int32_t *bt, const int32_t *seq_lens,
+                       int prefill_len, int hq, int hkv, int hd, int page, int max_blocks, float theta) {
+  struct alignas(VEC * sizeof(T)) Vec { T v[VEC]; };
+  __shared__ float2 csn[128];  // hd <= 256
   pdl_trigger();
   pdl_wait();
-  const int t = blockIdx.x, h = blockIdx.y, i = threadIdx.x;
+  const int t = blockIdx.x;
   const int b = prefill_len ? t / prefill_len : t;
   const int pos = seq_lens[b] + (prefill_len ? t % prefill_len : 0);
   const int half = hd / 2;
-  const T *src = qkv + (size_t)t * (hq + 2 * hkv) * hd + (size_t)h * hd;
-  if (i >= half) return;
-  if (h >= hq + hkv) {
-    T *dst = vc + page_index(bt, b, pos, max_blocks, page, hkv, h - hq - hkv, hd);
-    dst[i] = src[i];
-    dst[i + half] = src[i + half];
-    return;
+  for (int i = threadIdx.x; i < half; i += blockDim.x) {
+    const float inv_freq = 1.0f / powf(theta, (float)(2 * i) / (float)hd);
+    float sn, cs;
+    sincosf((float)pos * inv_freq, &sn, &cs);
+    csn[i] = make_float2(cs, sn);
   }
-  const float inv_freq = 1.0f / powf(theta, (float)(2 * i) / (float)hd);
-  const float ang = (float)pos * inv_freq;
-  float sn, cs;
-  sincosf(ang, &sn, &cs);
-  const float x1 = to_f32(src[i]);
-  const float x2 = to_f32(src[i + half]);
-  const float2 y = rope_rot(x1, x2, cs, sn);  // x * cos + rotate_half(x) * sin
-  const float y1 = y.x, y2 = y.y;
-  T *dst = h < hq ? q_out + ((size_t)t * hq + h) * hd
-                  : kc + page_index(bt, b, pos, max_blocks, page, hkv, h - hq, hd);
-  dst[i] = from_f32<T>(y1);
-  dst[i + half] = from_f32<T>(y2);
+  __syncthreads();
+  const int nh = hq + 2 * hkv, per = half / VEC;
+  const T *row = qkv + (size_t)t * nh * hd;
+  for (int task = threadIdx.x; task < nh * per; task += blockDim.x) {
+    const int h = task / per, i = (task % per) * VEC;
+    const Vec x1 = *reinterpret_cast<const Vec *>(row + (size_t)h * hd + i);
+    const Vec x2 = *reinterpret_cast<const Vec *>(row + (size_t)h * hd + half + i);
+    T *dst;
+    if (h >= hq + hkv) {
+      dst = vc + page_index(bt, b, pos, max_blocks, page, hkv, h - hq - hkv, hd);
+      *reinterpret_cast<Vec *>(dst + i) = x1;
+      *reinterpret_cast<Vec *>(dst + half + i) = x2;
+      continue;
+    }
+    dst = h < hq ? q_out + ((size_t)t * hq + h) * hd : kc + page_index(bt, b, pos, max_blocks, page, hkv, h - hq, hd);
+    Vec y1, y2;
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) {
+      const float2 c = csn[i + j];
+      const float2 y = rope_rot(to_f32(x1.v[j]), to_f32(x2.v[j]), c.x, c.y);  // x cos + rotate_half(x) sin
+      y1.v[j] = from_f32<T>(y.x);
+      y2.v[j] = from_f32<T>(y.y);
+    }
+    *reinterpret_cast<Vec *>(dst + i) = y1;
+    *reinterpret_cast<Vec *>(dst + half + i) = y2;
+  }
 }
 
 // ------------------------------------------------------------- decode
@@ -416,17 +434,20 @@ extern "C" int hx_rope_kv_append(const void *qkv, void *q_out, void *k_cache, vo
   if (n_tok == 0) return 0;
   if (!qkv || !q_out || !k_cache || !v_cache || !block_table || !seq_lens || hd % 2 || page_size <= 0)
     return HX_ERR_ARG;
+  if (hd > 256) return HX_ERR_UNSUPPORTED;
   cudaStream_t st = as_stream(stream);
-  dim3 grid(n_tok, hq + 2 * hkv);
-  const int threads = hd / 2 < 32 ? 32 : hd / 2;
-  if (dtype == HX_BF16)
-    return launch(rope_append_kernel<__nv_bfloat16>, dim3(grid), dim3(threads), 0, st, (const __nv_bfloat16 *)qkv, (__nv_bfloat16 *)q_out,
-                                              (__nv_bfloat16 *)k_cache, (__nv_bfloat16 *)v_cache, block_table,
-                                              seq_lens, prefill_len, hq, hkv, hd, page_size, max_blocks, theta);
-  else
-    return launch(rope_append_kernel<float>, dim3(grid), dim3(threads), 0, st, (const float *)qkv, (float *)q_out, (float *)k_cache,
-                                              (float *)v_cache, block_table, seq_lens, prefill_len, hq, hkv, hd,
-                                              page_size, max_blocks, theta);
+  const dim3 grid(n_tok);
+  const int half = hd / 2;
+#define HX_ROPE(T, V)                                                                                            \
+  return launch(rope_append_kernel<T, V>, grid, dim3(256), 0, st, (const T *)qkv, (T *)q_out, (T *)k_cache,     \
+                (T *)v_cache, block_table, seq_lens, prefill_len, hq, hkv, hd, page_size, max_blocks, theta)
+  if (dtype == HX_BF16) {
+    if (half % 4 == 0) HX_ROPE(__nv_bfloat16, 4);
+    HX_ROPE(__nv_bfloat16, 1);
+  }
+  if (half % 4 == 0) HX_ROPE(float, 4);
+  HX_ROPE(float, 1);
+#undef HX_ROPE
   return launch_status();
 }
 

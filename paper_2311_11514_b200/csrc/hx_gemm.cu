@@ -947,7 +947,15 @@ static Plan plan_gemm(int n_tok, int n_out, int K) {
 using namespace hx;
 
 // The stream-K decode GEMM is persistent: one CTA per SM (see launch_sk).
-static int sk_grid(int units) { return std::min(units, kNumSMs); }
+// persistent stream-K grid: one CTA per SM (HX_SK_CTAS overrides, e.g. 296 = 2 per SM)
+static int sk_ctas() {
+  static const int n = [] {
+    const char *e = getenv("HX_SK_CTAS");
+    return e ? atoi(e) : kNumSMs;
+  }();
+  return n;
+}
+static int sk_grid(int units) { return std::min(units, sk_ctas()); }
 
 // debug timeline: 8 u64 per stream-K CTA (start, dependency-wait done, end, smid,
 // seg0 accumulator ready, seg0 epilogue done, last-seg accumulator ready, #segments)
@@ -972,7 +980,7 @@ static int launch_sk(const CUtensorMap &mw, const CUtensorMap &mx, const SKArgs 
   // stream-K CTA lands on every SM: when two fit, the block scheduler may stack
   // two CTAs of the same launch on one SM (measured +0.11 ms per 7B decode step).
   // Smaller kernels (norms, attention) still co-reside under PDL.
-  constexpr size_t kOneCtaPerSm = 116 * 1024;
+  const size_t kOneCtaPerSm = sk_ctas() > kNumSMs ? 0 : 116 * 1024;
   const size_t smem = std::max<size_t>(kOneCtaPerSm, 1024 + STAGES * (BM * BK * 2 + BN * BK * 2) + (2 * STAGES + 4) * 8 + 32 +
                                                  (FUSED ? 128 * 17 * 4 : 0));
   static bool attr_done = false;
