@@ -1,0 +1,79 @@
+"""C5 (BASELINE configs[4]): SLO attainment vs Poisson request rate on 8xB200
+for the GA-chosen asymmetric plan vs homogeneous layouts, with every
+pipeline's service time MEASURED by this repo's engine (tools/measure_service.py)
+instead of the reference's closed-form cost model.
+
+    python tools/c5_report.py --plan ga/plan.json --svc svc_dir --out profiles/r01/c5_serving.json
+
+Tables (``{(replica, TaskSpec): s}``) are built per layout from the measured
+entries of each distinct pipeline shape; arrivals are the reference's
+``generate_workload`` Poisson traces (per-rate derived seeds, as
+``sweep_rate``); SLO = 2.0 x the measured latency of the fastest homogeneous
+single-request layout (one TP=4 pipeline of 80 layers), target 0.9.
+"""
+import argparse
+import json
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+from paper_2311_11514_b200 import planner as P
+from paper_2311_11514_b200.plan import plan_notation
+
+
+def table(plan, svc, task):
+    tab = {}
+    for r, pipe in enumerate(plan.pipelines):
+        key = (plan_notation(pipe), tuple(s.num_layers for s in pipe))
+        tab[(r, task)] = svc[key]
+    return tab
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--plan", required=True)
+    ap.add_argument("--svc", required=True)
+    ap.add_argument("--bundle", default=str(Path(__file__).resolve().parents[1] / "tests/golden/planner/b200_422/inputs"))
+    ap.add_argument("--out", required=True)
+    a = ap.parse_args()
+    b = Path(a.bundle)
+    cluster, model = P.load_cluster(b / "cluster.json"), P.load_model(b / "model.json")
+    wl = P.load_workload(b / "workload.json")
+    task = wl.dominant_task()
+    svc = {}
+    for f in sorted(Path(a.svc).glob("*.json")):
+        d = json.loads(f.read_text())
+        svc[(d["plan"], tuple(d["layers"]))] = d["seconds"]
+    layouts = {
+        "GA plan (b200 {4,2,2} buckets)": P.load_plan(a.plan),
+        "homogeneous 4 x [2] (GA plan, one bucket)": P.GlobalAssignment(tuple(
+            (P.StageAssignment((2 * i, 2 * i + 1), 80),) for i in range(4))),
+        "homogeneous 2 x [4]": P.GlobalAssignment(tuple(
+            (P.StageAssignment(tuple(range(4 * i, 4 * i + 4)), 80),) for i in range(2))),
+        "asymmetric 1 x [4,2,2] 40/20/20": P.GlobalAssignment(((P.StageAssignment((0, 1, 2, 3), 40),
+                                                                P.StageAssignment((4, 5), 20),
+                                                                P.StageAssignment((6, 7), 20)),)),
+    }
+    ref = svc[("[4]", (80,))]
+    slo = P.SloConfig(2.0, 0.9, ((task, ref),))
+    rates = [0.05, 0.1, 0.2, 0.3, 0.4, 0.5, 0.75, 1.0, 1.5, 2.0]
+    res = {"task": [task.batch_size, task.input_len, task.output_len], "slo_reference_s": ref, "slo_scale": 2.0,
+           "target": 0.9, "rates_rps": rates, "measured_service_s": {f"{k[0]} {list(k[1])}": v for k, v in svc.items()},
+           "layouts": {}}
+    for name, plan in layouts.items():
+        try:
+            tab = table(plan, svc, task)
+        except KeyError as exc:
+            res["layouts"][name] = {"missing_measurement": str(exc)}
+            continue
+        curve, peak = P.sweep_rate(plan, slo, rates, model, cluster, wl, service=tab)
+        res["layouts"][name] = {"pipelines": [plan_notation(p) for p in plan.pipelines],
+                                "attainment": [round(x, 4) for _, x in curve], "peak_rate_meeting_target": peak,
+                                "service_s": [tab[(r, task)] for r in range(len(plan.pipelines))]}
+    Path(a.out).write_text(json.dumps(res, indent=1) + "\n")
+    print(json.dumps(res, indent=1))
+
+
+if __name__ == "__main__":
+    main()
