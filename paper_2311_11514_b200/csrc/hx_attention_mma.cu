@@ -11,6 +11,8 @@
 //     merged in smem, splits through the workspace (last-CTA ticket).
 // Both are HBM/L2-bound on K/V; fp32 mode and MHA decode use the CUDA-core
 // kernels in hx_attention.cu.
+#include <cstdlib>
+
 #include "hx_common.cuh"
 
 namespace hx {
@@ -391,7 +393,7 @@ __device__ __forceinline__ uint32_t sw128_addr(uint32_t base, int r, int col) {
   return base + half * 8192 + r * 128 + ((chunk ^ (r & 7)) << 4) + ((col & 7) << 1);
 }
 
-template <int G, bool ROPE, int NS, int BPI>
+template <int G, bool ROPE, int NS, int BPI, bool CL>
 __global__ void __launch_bounds__(AM_THREADS * BPI)
     attn_decode_tma_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
                            const __nv_bfloat16 *q, const int32_t *bt, const int32_t *seq_lens, __nv_bfloat16 *o,
@@ -405,10 +407,16 @@ __global__ void __launch_bounds__(AM_THREADS * BPI)
   __nv_bfloat16 *qs = reinterpret_cast<__nv_bfloat16 *>(ring + NS * 2 * BLK);
   uint64_t *full = reinterpret_cast<uint64_t *>(qs + 16 * LD);
   float *red = reinterpret_cast<float *>(ring);  // [4 warps][16][HD + 2], reuses the ring at the end
+  float *mypart = red + 4 * BPI * 16 * (HD + 2);  // [G][HD + 2] this split's combined partial (CL)
   __shared__ int s_last;
   pdl_trigger();
-  const int b = blockIdx.x / hkv, kvh = blockIdx.x % hkv;
-  const int split = blockIdx.y, splits = gridDim.y;
+  // CL: the splits of one (batch, kv-head) pair form a thread-block cluster and
+  // combine through DSMEM; otherwise grid.y = splits and the last split to
+  // finish (ticket) combines through the workspace
+  const int splits = CL ? (int)cluster_nctarank() : (int)gridDim.y;
+  const int split = CL ? (int)cluster_rank() : (int)blockIdx.y;
+  const int pidx = CL ? (int)blockIdx.x / splits : (int)blockIdx.x;
+  const int b = pidx / hkv, kvh = pidx % hkv;
   const int hq = hkv * G;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t4 = lane & 3;
@@ -590,12 +598,33 @@ __global__ void __launch_bounds__(AM_THREADS * BPI)
     if (splits == 1) {
       o[((size_t)b * hq + kvh * G + r) * HD + d] = __float2bfloat16_rn(A / L);
     } else {
-      float *part = ws + ((pair * splits + split) * G + r) * (HD + 2);
+      float *part = CL ? mypart + r * (HD + 2) : ws + ((pair * splits + split) * G + r) * (HD + 2);
       part[d] = A;
       if (d == 0) { part[HD] = M; part[HD + 1] = L; }
     }
   }
   if (splits == 1) return;
+  if constexpr (CL) {
+    // every split's (A, M, L) sits in its own smem: combine across the cluster
+    // over DSMEM, each CTA producing an interleaved 1/splits of the outputs
+    cluster_sync_all();
+    for (int w = split * AM_THREADS * BPI + threadIdx.x; w < G * HD; w += splits * AM_THREADS * BPI) {
+      const int r = w / HD, d = w % HD;
+      float M = -INFINITY;
+      for (int c2 = 0; c2 < splits; ++c2) M = fmaxf(M, dsmem_ld_f32(mypart + r * (HD + 2) + HD, c2));
+      float L = 0.f, A = 0.f;
+      for (int c2 = 0; c2 < splits; ++c2) {
+        const float ms = dsmem_ld_f32(mypart + r * (HD + 2) + HD, c2);
+        if (ms == -INFINITY) continue;
+        const float cf = exp2f(ms - M);
+        L += dsmem_ld_f32(mypart + r * (HD + 2) + HD + 1, c2) * cf;
+        A += dsmem_ld_f32(mypart + r * (HD + 2) + d, c2) * cf;
+      }
+      o[((size_t)b * hq + kvh * G + r) * HD + d] = __float2bfloat16_rn(A / L);
+    }
+    cluster_sync_all();  // peers have read this CTA's partial before it exits
+    return;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     const int tk = ticket_acq_rel(&counters[pair]);
@@ -648,20 +677,29 @@ __global__ void __launch_bounds__(AM_THREADS * BPI)
   }
 }
 
-template <int G, bool ROPE, int NS, int BPI>
+template <int G, bool ROPE, int NS, int BPI, bool CL = false>
 static int launch_decode_tma_g(dim3 grid, const CUtensorMap &mk, const CUtensorMap &mv, const void *q,
                                const int32_t *bt, const int32_t *sl, void *o, int hkv, int maxb, float *ws, int *cnt,
                                void *kc, void *vc, float theta, cudaStream_t st) {
   const size_t smem = 1024 + NS * 2 * 16384 + 16 * 136 * 2 + NS * 8 + 16;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(attn_decode_tma_kernel<G, ROPE, NS, BPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(attn_decode_tma_kernel<G, ROPE, NS, BPI, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
   const float sl2 = 1.4426950408889634f / sqrtf(128.f);
-  return launch(attn_decode_tma_kernel<G, ROPE, NS, BPI>, grid, dim3(AM_THREADS * BPI), smem, st, mk, mv, (const __nv_bfloat16 *)q,
+  if constexpr (CL)
+    return launch_cluster(attn_decode_tma_kernel<G, ROPE, NS, BPI, CL>, dim3(grid.x * grid.y), dim3(AM_THREADS * BPI),
+                          smem, st, (int)grid.y, mk, mv, (const __nv_bfloat16 *)q, bt, sl, (__nv_bfloat16 *)o, hkv, maxb,
+                          sl2, ws, cnt, (__nv_bfloat16 *)kc, (__nv_bfloat16 *)vc, theta);
+  return launch(attn_decode_tma_kernel<G, ROPE, NS, BPI, CL>, grid, dim3(AM_THREADS * BPI), smem, st, mk, mv, (const __nv_bfloat16 *)q,
                 bt, sl, (__nv_bfloat16 *)o, hkv, maxb, sl2, ws, cnt, (__nv_bfloat16 *)kc, (__nv_bfloat16 *)vc, theta);
 }
+
+static const int g_attn_cluster = [] {  // split-KV combine over DSMEM clusters (HX_ATTN_CLUSTER=0: workspace)
+  const char *e = getenv("HX_ATTN_CLUSTER");
+  return e ? atoi(e) : 1;
+}();
 
 // kc/vc: [num_blocks][hkv][64][128] bf16. rope: q is the packed qkv row and the
 // new token's k (rotated) and v are appended by the kernel itself.
@@ -680,6 +718,9 @@ int launch_decode_tma(int G, dim3 grid, const void *q, const void *kc, const voi
   if (ns == 6)                                                                                                     \
     return rope ? launch_decode_tma_g<GG, true, 6, 2>(grid, mk, mv, q, bt, sl, o, hkv, maxb, ws, cnt, k, v, theta, st) \
                 : launch_decode_tma_g<GG, false, 6, 2>(grid, mk, mv, q, bt, sl, o, hkv, maxb, ws, cnt, k, v, theta, st); \
+  if (grid.y >= 2 && grid.y <= 8 && g_attn_cluster)                                                               \
+    return rope ? launch_decode_tma_g<GG, true, 3, 1, true>(grid, mk, mv, q, bt, sl, o, hkv, maxb, ws, cnt, k, v, theta, st) \
+                : launch_decode_tma_g<GG, false, 3, 1, true>(grid, mk, mv, q, bt, sl, o, hkv, maxb, ws, cnt, k, v, theta, st); \
   return rope ? launch_decode_tma_g<GG, true, 3, 1>(grid, mk, mv, q, bt, sl, o, hkv, maxb, ws, cnt, k, v, theta, st)   \
               : launch_decode_tma_g<GG, false, 3, 1>(grid, mk, mv, q, bt, sl, o, hkv, maxb, ws, cnt, k, v, theta, st)
   switch (G) {

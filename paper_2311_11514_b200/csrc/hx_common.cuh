@@ -77,6 +77,11 @@ inline int launch_cluster(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t 
 }
 
 // cluster helpers: rank in cluster, DSMEM read of another CTA's shared float, cluster barrier
+__device__ __forceinline__ unsigned cluster_nctarank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
 __device__ __forceinline__ unsigned cluster_rank() {
   unsigned r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));

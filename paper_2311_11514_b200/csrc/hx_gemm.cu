@@ -364,6 +364,7 @@ struct SKArgs {
   int *counters;
   unsigned long long *trace;  // optional per-CTA timeline (hx_debug_trace): start, wait done, end, smid
   int l2pf;                   // weight tiles beyond the smem ring prefetched into L2 before the PDL wait
+  const uint8_t *w_ptr;       // packed weights (for the epilogue warps' L2 prefetch)
   EpiArgs epi;
 };
 
@@ -528,14 +529,6 @@ __global__ void __launch_bounds__(192, 2)
         mbar_arrive_expect_tx(&full[i], A_BYTES + B_BYTES);
         load_w(i, u0 + i);
       }
-      // ...and the next l2pf tiles into L2, so HBM keeps streaming this GEMM's
-      // weights while the previous kernel (all-reduce, norm, attention tail)
-      // is latency-bound; after the wait those tiles arrive at L2 speed
-      for (int i = pre; i < min(n, pre + p.l2pf); ++i) {
-        const int u = u0 + i;
-        if (p.w_packed) tma_prefetch_l2_2d(&tm_w, 0, u * BM);
-        else tma_prefetch_l2_2d(&tm_w, (u % p.KB) * BK, (u / p.KB) * BM);
-      }
       pdl_wait();
       if (p.trace) p.trace[8 * c + 1] = globaltimer();
       for (int i = 0; i < pre; ++i) load_x(i, u0 + i);
@@ -577,6 +570,19 @@ __global__ void __launch_bounds__(192, 2)
     const int q = warp & 3;
     const int row = q * 32 + lane;
     const int etid = threadIdx.x - 64;  // 0..127
+    // Idle until the first accumulator: pull the weight tiles beyond the
+    // producer's smem ring into L2 (plain LSU prefetches, so they never queue
+    // in front of the TMA loads the MMA waits for), letting HBM stream this
+    // GEMM's weights while the previous kernel (norm, all-reduce) is short of
+    // bytes; after the PDL wait those tiles arrive at L2 speed.
+    if (p.l2pf && p.w_packed) {
+      const int i0 = min(u1 - u0, STAGES), i1 = min(u1 - u0, STAGES + p.l2pf);
+      constexpr int LINES = BM * BK * 2 / 128;  // 128 B lines per 16 KB tile
+      for (int l = etid; l < (i1 - i0) * LINES; l += 128) {
+        const uint8_t *a = p.w_ptr + (size_t)(u0 + i0 + l / LINES) * (BM * BK * 2) + (l % LINES) * 128;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+      }
+    }
     int seg = 0;
     for (int u = u0; u < u1; ++seg) {
       const int t = u / p.KB;
@@ -1128,7 +1134,12 @@ static int linear_impl(const void *w, const void *x, void *y, int dtype, int y_d
       const char *e = getenv("HX_GEMM_L2PF");
       return e ? atoi(e) : 16;
     }();
-    sk.l2pf = (flags & HX_LINEAR_L2_PREFETCH) ? l2pf : 0;
+    static const int l2pf_all = [] {
+      const char *e = getenv("HX_GEMM_L2PF_ALL");
+      return e ? atoi(e) : 0;
+    }();
+    sk.l2pf = ((flags & HX_LINEAR_L2_PREFETCH) || l2pf_all) ? l2pf : 0;
+    sk.w_ptr = reinterpret_cast<const uint8_t *>(w);
     sk.c = y; sk.ldm = 1; sk.ldn = ldy; sk.M = n_out; sk.N = n_tok;
     sk.c_bf16 = p.c_bf16; sk.accumulate = accumulate; sk.w_packed = packed; sk.epi = epi;
     sk.defer = (flags & HX_LINEAR_DEFER_REDUCE) ? 1 : 0;

@@ -347,6 +347,37 @@ def test_decode_rope_append_fused_bit_identical(hq, hkv, ctx, b):
     assert torch.equal(o_fused, o_sep)
 
 
+@pytest.mark.parametrize("b,hq,hkv,ctx", [(32, 32, 4, 1100), (16, 16, 2, 700), (12, 32, 4, 500), (8, 64, 8, 1279)])
+def test_decode_attention_cluster_split_combine(b, hq, hkv, ctx):
+    """(batch, kv-head) pair counts that give 2-8 KV splits: the splits of a
+    pair run as one thread-block cluster and combine over DSMEM. Checked
+    against the torch reference, and fused (RoPE + append) == separate."""
+    dt, hd, page = torch.bfloat16, 128, 64
+    kc, vc, bt, g = _paged_setup(dt, b, hq, hkv, hd, page, ctx + 1)
+    n = (hq + 2 * hkv) * hd
+    seq = torch.zeros(b, dtype=torch.int32, device=DEV)
+    hist = torch.randn(b * ctx, n, device=DEV, generator=g).to(dt)
+    ops.rope_kv_append(hist, torch.empty(b * ctx, hq * hd, device=DEV, dtype=dt), kc, vc, bt, seq, b * ctx, ctx,
+                       hq, hkv, hd, 10000.0)
+    seq.copy_(torch.tensor([max(1, ctx - 37 * i) for i in range(b)], dtype=torch.int32))
+    kr, vr = kc.clone(), vc.clone()
+    new = torch.randn(b, n, device=DEV, generator=g).to(dt)
+    q, qr = (torch.empty(b, hq * hd, device=DEV, dtype=dt) for _ in range(2))
+    ws = torch.zeros(ops.attn_decode_workspace(b, hq, hkv, hd, ctx + 1) // 4 + 64, dtype=torch.int32, device=DEV)
+    k2, v2 = kc.clone(), vc.clone()
+    ops.rope_kv_append(new, q, kc, vc, bt, seq, b, 0, hq, hkv, hd, 10000.0)
+    ref.rope_kv_append(new, qr, kr, vr, bt, seq, b, 0, hq, hkv, hd, 10000.0)
+    o = torch.empty(b, hq * hd, device=DEV, dtype=dt)
+    want = torch.empty(b, hq * hd, device=DEV)
+    ops.attn_decode(q, kc, vc, bt, seq, o, b, hq, hkv, hd, ctx + 1, ws)
+    ref.attn_decode(qr, kr, vr, bt, seq, want, b, hq, hkv, hd, ctx + 1)
+    o_fused = torch.empty_like(o)
+    ops.attn_decode_rope_append(new, k2, v2, bt, seq, o_fused, b, hq, hkv, hd, ctx + 1, 10000.0, ws)
+    torch.cuda.synchronize()
+    assert rel_err(o, want) < 2e-2
+    assert torch.equal(o_fused, o)
+
+
 def test_decode_rope_append_fused_unsupported_shapes():
     assert not ops.decode_rope_fusable(torch.float32, 128, 64, 8, 8)
     assert not ops.decode_rope_fusable(torch.bfloat16, 64, 64, 8, 8)
