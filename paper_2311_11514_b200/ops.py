@@ -9,6 +9,7 @@ raise (``HxError``); the data path has no CPU or eager-PyTorch substitute.
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 import torch
@@ -80,7 +81,7 @@ def load(path: Path | str | None = None):
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    p = Path(path) if path else Path(os.environ.get("HX_LIB", LIB_PATH))
     if not p.exists():
         raise HxError(f"{p} not built -- run `python -m paper_2311_11514_b200.build` "
                       "(there is no CPU fallback for the data path)")
