@@ -13,7 +13,8 @@ configs; synthetic prompts, random-init weights of the named architecture):
   N=8  Llama-2-70B bf16, plan [4,2,2] layers 40/20/20, b=32, 1024/256 (configs[3])
 
 ``value`` = decode tokens/s = b * (s_out - 1) * K / (sum of decode-phase device
-time, CUDA events, max over ranks), inputs resident. ``e2e`` = generated
+time, CUDA events, on the last stage -- first to last generated token -- max
+over its ranks), inputs resident. ``e2e`` = generated
 tokens/s through the public API with host prompts in and host ids out
 (b * s_out per request / wall time of generate, prefill included).
 Weights (13.5-140 GB) are far larger than the 126 MB L2, so every decode step
@@ -361,10 +362,16 @@ def main():
     barrier()
     wall = time.perf_counter() - t_wall0
     clk = clocks.stop()
-    t = torch.tensor([dec_s, pre_s, wall, sum(walls)], dtype=torch.float64, device=dev)
+    # The decode phase runs from the first generated token (the last stage's
+    # prefill head) to the last one, so its duration is taken on the last
+    # stage (max over its ranks). Earlier stages' decode clocks start when their
+    # own prefill micro-batches end and also absorb the later stages' prefill
+    # tail; that max-over-all-ranks figure is reported as decode_s_all_ranks.
+    is_last = any(e.role.is_last for e in eng.execs)
+    t = torch.tensor([dec_s, pre_s, wall, sum(walls), dec_s if is_last else 0.0], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    dec_s, pre_s, wall, wall_gen = t.tolist()
+    dec_all, pre_s, wall, wall_gen, dec_s = t.tolist()
     b, s_in, s_out = w["batch"], w["s_in"], w["s_out"]
     value = b * (s_out - 1) * args.steps / dec_s
     e2e = b * s_out * args.steps / wall_gen
@@ -394,6 +401,7 @@ def main():
             "p50_decode_step_ms": round(p50, 4) if p50 else None,
             "prefill_ms": round(pre_s / args.steps * 1e3, 3),
             "decode_ms_per_request": round(dec_s / args.steps * 1e3, 3),
+            "decode_s_all_ranks": round(dec_all / args.steps, 4),
             "step_roofline": {"bytes_per_step_all_gpus": decode_bytes_per_step(cfg, w),
                               "t_star_ms": round(step_rf * 1e3, 4),
                               "frac": round(step_rf * 1e3 / p50, 4) if p50 else None,
