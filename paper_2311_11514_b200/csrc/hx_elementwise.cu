@@ -16,7 +16,10 @@ void set_max_carveout(const void *fn) {
   if (e && atoi(e) == 0) return;
   cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
 }
-int g_pdl = 1;
+int g_pdl = [] {  // HX_PDL=0 turns programmatic dependent launch off (A/B)
+  const char *e = getenv("HX_PDL");
+  return e ? atoi(e) : 1;
+}();
 
 constexpr int ROW_THREADS = 256;
 
