@@ -27,13 +27,13 @@ struct AttnSmem {
 };
 
 // gather a 64-key block of K and V rows (positions p0 + k0 ..) into smem
-template <int HD>
+template <int HD, int THREADS = AM_THREADS>
 __device__ __forceinline__ void load_kv_block(__nv_bfloat16 *ks, __nv_bfloat16 *vs, const __nv_bfloat16 *kc,
                                               const __nv_bfloat16 *vc, const int32_t *btb, int p0, int k0,
                                               int klim, int page, int hkv, int kvh) {
   constexpr int LD = AttnSmem<HD>::LD;
   constexpr int CH = HD / 8;  // 16-byte chunks per row
-  for (int i = threadIdx.x; i < AM_BKV * CH; i += AM_THREADS) {
+  for (int i = threadIdx.x; i < AM_BKV * CH; i += THREADS) {
     const int r = i / CH, c = (i % CH) * 8;
     const int kj = k0 + r;
     __nv_bfloat16 *kd = ks + r * LD + c, *vd = vs + r * LD + c;
@@ -128,8 +128,11 @@ __device__ __forceinline__ void online_softmax(float (*s)[4], float (*o)[4], flo
 }
 
 // ------------------------------------------------------------------ prefill
-template <int HD>
-__global__ void __launch_bounds__(AM_THREADS)
+// NW warps x 16 query rows per CTA (BQ = 16 NW); K/V 64-key blocks double
+// buffered with cp.async and shared by all NW warps (NW = 8: half the K/V smem
+// traffic per query row of NW = 4, 16 warps per SM at 2 CTAs/SM)
+template <int HD, int NW>
+__global__ void __launch_bounds__(32 * NW)
     attn_prefill_mma_kernel(const __nv_bfloat16 *q, const __nv_bfloat16 *kc, const __nv_bfloat16 *vc,
                             const int32_t *bt, const int32_t *seq_lens, __nv_bfloat16 *o, int s_len, int hq,
                             int hkv, int page, int max_blocks, float sl2) {
@@ -138,20 +141,21 @@ __global__ void __launch_bounds__(AM_THREADS)
   constexpr int LD = AttnSmem<HD>::LD;
   extern __shared__ __align__(128) uint8_t smraw[];
   __nv_bfloat16 *qs = reinterpret_cast<__nv_bfloat16 *>(smraw);
-  __nv_bfloat16 *ks = qs + AM_BQ * LD;  // [2][BKV][LD]
+  constexpr int BQ = 16 * NW, THREADS = 32 * NW;
+  __nv_bfloat16 *ks = qs + BQ * LD;  // [2][BKV][LD]
   __nv_bfloat16 *vs = ks + 2 * AttnSmem<HD>::TILE;
   const int nqt = gridDim.x;
   const int qt = nqt - 1 - blockIdx.x;  // heaviest (last) query tiles first
   const int h = blockIdx.y, b = blockIdx.z;
   const int kvh = h / (hq / hkv);
   const int p0 = seq_lens[b];
-  const int q0 = qt * AM_BQ;
+  const int q0 = qt * BQ;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t4 = lane & 3;
   const int32_t *btb = bt + (size_t)b * max_blocks;
 
   constexpr int CH = HD / 8;
-  for (int i = threadIdx.x; i < AM_BQ * CH; i += AM_THREADS) {
+  for (int i = threadIdx.x; i < BQ * CH; i += THREADS) {
     const int r = i / CH, c = (i % CH) * 8;
     __nv_bfloat16 *d = qs + r * LD + c;
     if (q0 + r < s_len)
@@ -159,9 +163,9 @@ __global__ void __launch_bounds__(AM_THREADS)
     else
       *reinterpret_cast<uint4 *>(d) = make_uint4(0, 0, 0, 0);
   }
-  const int q_hi = min(s_len, q0 + AM_BQ);
+  const int q_hi = min(s_len, q0 + BQ);
   const int nblk = (q_hi + AM_BKV - 1) / AM_BKV;
-  load_kv_block<HD>(ks, vs, kc, vc, btb, p0, 0, s_len, page, hkv, kvh);
+  load_kv_block<HD, THREADS>(ks, vs, kc, vc, btb, p0, 0, s_len, page, hkv, kvh);
   cp_async_commit();
 
   uint32_t qf[HD / 16][4];
@@ -176,7 +180,7 @@ __global__ void __launch_bounds__(AM_THREADS)
   for (int kb = 0; kb < nblk; ++kb) {
     const int buf = kb & 1;
     if (kb + 1 < nblk) {
-      load_kv_block<HD>(ks + (buf ^ 1) * AttnSmem<HD>::TILE, vs + (buf ^ 1) * AttnSmem<HD>::TILE, kc, vc, btb, p0,
+      load_kv_block<HD, THREADS>(ks + (buf ^ 1) * AttnSmem<HD>::TILE, vs + (buf ^ 1) * AttnSmem<HD>::TILE, kc, vc, btb, p0,
                         (kb + 1) * AM_BKV, s_len, page, hkv, kvh);
     }
     cp_async_commit();
@@ -734,9 +738,9 @@ int launch_decode_tma(int G, dim3 grid, const void *q, const void *kc, const voi
   return HX_ERR_UNSUPPORTED;
 }
 
-template <int HD>
+template <int HD, int NW>
 static size_t prefill_smem() {
-  return sizeof(__nv_bfloat16) * (AM_BQ * AttnSmem<HD>::LD + 4 * AttnSmem<HD>::TILE);
+  return sizeof(__nv_bfloat16) * (16 * NW * AttnSmem<HD>::LD + 4 * AttnSmem<HD>::TILE);
 }
 template <int HD>
 static size_t decode_smem() {
@@ -745,26 +749,35 @@ static size_t decode_smem() {
   return sizeof(__nv_bfloat16) * (16 * AttnSmem<HD>::LD + 2 * DEC_NS * AttnSmem<HD>::TILE);
 }
 
-template <int HD>
+template <int HD, int NW>
 static int launch_prefill_mma_hd(const void *q, const void *kc, const void *vc, const int32_t *bt, const int32_t *sl,
                                  void *o, int batch, int s, int hq, int hkv, int page, int maxb, cudaStream_t st) {
-  const size_t smem = prefill_smem<HD>();
+  const size_t smem = prefill_smem<HD, NW>();
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(attn_prefill_mma_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(attn_prefill_mma_kernel<HD, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
   const float sl2 = 1.4426950408889634f / sqrtf((float)HD);
-  dim3 grid((s + AM_BQ - 1) / AM_BQ, hq, batch);
-  return launch(attn_prefill_mma_kernel<HD>, grid, dim3(AM_THREADS), smem, st, (const __nv_bfloat16 *)q,
+  dim3 grid((s + 16 * NW - 1) / (16 * NW), hq, batch);
+  return launch(attn_prefill_mma_kernel<HD, NW>, grid, dim3(32 * NW), smem, st, (const __nv_bfloat16 *)q,
                 (const __nv_bfloat16 *)kc, (const __nv_bfloat16 *)vc, bt, sl, (__nv_bfloat16 *)o, s, hq, hkv, page,
                 maxb, sl2);
 }
 
+static const int g_pf_warps = [] {  // prefill attention warps per CTA (HX_PF_WARPS=4 | 8)
+  const char *e = getenv("HX_PF_WARPS");
+  return e ? atoi(e) : 8;
+}();
+
 int launch_prefill_mma(const void *q, const void *kc, const void *vc, const int32_t *bt, const int32_t *sl, void *o,
                        int batch, int s, int hq, int hkv, int hd, int page, int maxb, cudaStream_t st) {
-  if (hd == 128) return launch_prefill_mma_hd<128>(q, kc, vc, bt, sl, o, batch, s, hq, hkv, page, maxb, st);
-  if (hd == 64) return launch_prefill_mma_hd<64>(q, kc, vc, bt, sl, o, batch, s, hq, hkv, page, maxb, st);
+  if (hd == 128)
+    return g_pf_warps == 4 ? launch_prefill_mma_hd<128, 4>(q, kc, vc, bt, sl, o, batch, s, hq, hkv, page, maxb, st)
+                           : launch_prefill_mma_hd<128, 8>(q, kc, vc, bt, sl, o, batch, s, hq, hkv, page, maxb, st);
+  if (hd == 64)
+    return g_pf_warps == 4 ? launch_prefill_mma_hd<64, 4>(q, kc, vc, bt, sl, o, batch, s, hq, hkv, page, maxb, st)
+                           : launch_prefill_mma_hd<64, 8>(q, kc, vc, bt, sl, o, batch, s, hq, hkv, page, maxb, st);
   return HX_ERR_UNSUPPORTED;
 }
 
