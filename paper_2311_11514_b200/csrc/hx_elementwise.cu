@@ -97,8 +97,8 @@ __global__ void __launch_bounds__(ROW_THREADS)
   for (int r = 0; r < MAXV; ++r) {
     const int i = (r * ROW_THREADS + threadIdx.x) * 4;
     if (i < hidden) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) o[i + j] = from_f32<TO>((v[r][j] * inv) * g[r][j]);
+      store4(o + i, (v[r][0] * inv) * g[r][0], (v[r][1] * inv) * g[r][1], (v[r][2] * inv) * g[r][2],
+             (v[r][3] * inv) * g[r][3]);
     }
   }
 }
