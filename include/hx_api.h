@@ -189,6 +189,18 @@ int hx_handoff_push(const void *src, void *const *dst_inboxes, int n_dst, size_t
 int hx_handoff_pull(void *dst, void *inbox, size_t words, size_t max_words, int *state,
                     hx_stream_t stream);
 
+/* ---- Prefill attention on tcgen05 (whole prompt, no earlier context).
+ * hx_prefill_vt writes the prompt's V transposed per (sequence, kv head):
+ * vt[((b * hkv + h) * 128 + d) * s + i] (bf16) from the packed qkv rows.
+ * hx_attn_prefill_tc: o[b, i, h, :] = causal softmax(q k^T / sqrt(128)) v with q
+ * [b*s][hq*128] (roped), K from the paged cache (page 64), V from vt; needs hd
+ * 128, s % 128 == 0 (HX_ERR_UNSUPPORTED otherwise: use hx_attn_prefill). */
+int hx_prefill_vt(const void *qkv, void *vt, int batch, int s_len, int hq, int hkv, int hd,
+                  hx_stream_t stream);
+int hx_attn_prefill_tc(const void *q, const void *k_cache, const void *vt, const int32_t *block_table,
+                       void *o, int batch, int s_len, int hq, int hkv, int hd, int page_size,
+                       int max_blocks, hx_stream_t stream);
+
 /* out[t, j] = silu(gu[t, j]) * gu[t, inter + j], j < inter */
 int hx_swiglu(const void *gu, void *out, int dtype, int n_tok, int inter,
               hx_stream_t stream);

@@ -236,6 +236,11 @@ class RankExecutor:
         self.par = None          # ops.PeerAllReduce when TP>1 ranks run in separate processes
         self._peer_now = False
         self.attn_ws = torch.zeros(max(self.attn_ws_bytes, 256) // 4 + 64, dtype=torch.int32, device=dev)
+        # tcgen05 prefill attention (default; HX_PREFILL_TC=0 selects the mma.sync
+        # kernel): needs V transposed per (sequence, kv head) -- a prefill-only scratch
+        self.tc_prefill = (os.environ.get("HX_PREFILL_TC", "1") == "1" and dtype == torch.bfloat16
+                           and dev.type == "cuda" and self.k is _ops and self.hd == 128 and page_size == 64)
+        self.vt = z(batch * max_prompt * self.hkv * self.hd) if self.tc_prefill else None
         self._x_full = self.x
         self.bt, self.sl = self.kv.block_table, self.kv.seq_lens   # the current micro-batch's sequences
 
@@ -268,7 +273,11 @@ class RankExecutor:
             k.linear(lw["wqkv"], self.h, self.qkv, n_tok, self.lin_ws)
             k.rope_kv_append(self.qkv, self.q, kc, vc, self.bt, self.sl, n_tok,
                              prefill_len, self.hq, self.hkv, self.hd, cfg.rope_theta)
-        if prefill_len:
+        if prefill_len and self.tc_prefill and prefill_len % 128 == 0:
+            nb = n_tok // prefill_len
+            k.prefill_vt(self.qkv, self.vt, nb, prefill_len, self.hq, self.hkv, self.hd)
+            k.attn_prefill_tc(self.q, kc, self.vt, self.bt, self.attn, nb, prefill_len, self.hq, self.hkv, self.hd)
+        elif prefill_len:
             k.attn_prefill(self.q, kc, vc, self.bt, self.sl, self.attn,
                            n_tok // prefill_len, prefill_len, self.hq, self.hkv, self.hd)
         elif not self.rope_in_attn:

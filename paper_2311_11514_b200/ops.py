@@ -57,6 +57,8 @@ _SIGS = {
     "hx_handoff_inbox_init": ([_P, _SZ, _P], _I),
     "hx_handoff_push": ([_P, ctypes.POINTER(ctypes.c_void_p), _I, _SZ, _SZ, _P, _P], _I),
     "hx_handoff_pull": ([_P, _P, _SZ, _SZ, _P, _P], _I),
+    "hx_prefill_vt": ([_P, _P, _I, _I, _I, _I, _I, _P], _I),
+    "hx_attn_prefill_tc": ([_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P], _I),
     "hx_swiglu": ([_P, _P, _I, _I, _I, _P], _I),
     "hx_rope_kv_append": ([_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _F, _P], _I),
     "hx_attn_decode_paged": ([_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _SZ, _P], _I),
@@ -302,6 +304,17 @@ def attn_prefill(q, k_cache, v_cache, block_table, seq_lens, o, batch, s, hq, hk
     _check(load().hx_attn_prefill(_p(q), _p(k_cache), _p(v_cache), _p(block_table), _p(seq_lens), _p(o),
                                   dtype_code(q.dtype), batch, s, hq, hkv, hd, k_cache.shape[2],
                                   block_table.shape[1], _stream()), "hx_attn_prefill")
+
+
+def prefill_vt(qkv, vt, batch, s, hq, hkv, hd):
+    """V of the prompt, transposed per (sequence, kv head), for attn_prefill_tc."""
+    _check(load().hx_prefill_vt(_p(qkv), _p(vt), batch, s, hq, hkv, hd, _stream()), "hx_prefill_vt")
+
+
+def attn_prefill_tc(q, k_cache, vt, block_table, o, batch, s, hq, hkv, hd):
+    """Causal prefill attention on tcgen05 (hd 128, s % 128 == 0, page 64, no earlier context)."""
+    _check(load().hx_attn_prefill_tc(_p(q), _p(k_cache), _p(vt), _p(block_table), _p(o), batch, s, hq, hkv, hd,
+                                     k_cache.shape[2], block_table.shape[1], _stream()), "hx_attn_prefill_tc")
 
 
 def advance(seq_lens, batch, n):

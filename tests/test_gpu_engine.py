@@ -97,6 +97,13 @@ def test_llama7b_shape_bf16_two_layers(fuse, monkeypatch):
     _bf16_check(cfg, [1], [2], 8, 64, 6)
 
 
+def test_llama7b_shape_bf16_tcgen05_prefill_attention(monkeypatch):
+    """Prompt of 128 tokens: the prefill attention runs on the tcgen05 kernel."""
+    monkeypatch.setenv("HX_PREFILL_TC", "1")
+    cfg = preset("llama2-7b", num_layers=2)
+    _bf16_check(cfg, [1], [2], 4, 128, 6)
+
+
 @pytest.mark.parametrize("fuse", FUSIONS)
 def test_gqa_asymmetric_bf16(fuse, monkeypatch):
     """GQA group 8 per rank (70B-style head ratio) under an asymmetric [2,1] plan."""

@@ -408,3 +408,26 @@ def test_prefill_attention(dt, hq, hkv, hd, s):
     ref.attn_prefill(q, kc, vc, bt, seq, want, b, s, hq, hkv, hd)
     torch.cuda.synchronize()
     assert rel_err(o, want) < (2e-5 if dt == torch.float32 else 2e-2)
+
+
+@pytest.mark.parametrize("b,s,hq,hkv", [(2, 128, 4, 4), (2, 256, 8, 2), (1, 512, 8, 1), (3, 384, 16, 8)])
+def test_prefill_attention_tcgen05(b, s, hq, hkv):
+    """tcgen05 causal prefill attention (TMEM S/PV accumulators, P through smem)
+    against the torch fp32 reference on the same paged K and roped q."""
+    dt, hd, page = torch.bfloat16, 128, 64
+    kc, vc, bt, g = _paged_setup(dt, b, hq, hkv, hd, page, s, seed=3)
+    seq = torch.zeros(b, dtype=torch.int32, device=DEV)
+    qkv = torch.randn(b * s, (hq + 2 * hkv) * hd, device=DEV, generator=g).to(dt)
+    q = torch.empty(b * s, hq * hd, device=DEV, dtype=dt)
+    ops.rope_kv_append(qkv, q, kc, vc, bt, seq, b * s, s, hq, hkv, hd, 10000.0)
+    vt = torch.empty(b * hkv * hd * s, device=DEV, dtype=dt)
+    ops.prefill_vt(qkv, vt, b, s, hq, hkv, hd)
+    o = torch.empty(b * s, hq * hd, device=DEV, dtype=dt)
+    ops.attn_prefill_tc(q, kc, vt, bt, o, b, s, hq, hkv, hd)
+    want = torch.empty(b * s, hq * hd, device=DEV)
+    ref.attn_prefill(q, kc, vc, bt, seq, want, b, s, hq, hkv, hd)
+    # vt is V transposed per (sequence, kv head)
+    v = qkv.view(b, s, hq + 2 * hkv, hd)[:, :, hq + hkv:].float()
+    assert torch.equal(vt.view(b, hkv, hd, s).float(), v.permute(0, 2, 3, 1))
+    torch.cuda.synchronize()
+    assert rel_err(o, want) < 2e-2

@@ -26,19 +26,25 @@ def main():
         sl = torch.zeros(b, dtype=torch.int32, device="cuda")
         q = torch.randn(b * s, hq * hd, device="cuda").bfloat16()
         o = torch.empty_like(q)
-        for _ in range(2):
-            ops.attn_prefill(q, kc, vc, bt, sl, o, b, s, hq, hkv, hd)
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(10):
-            ops.attn_prefill(q, kc, vc, bt, sl, o, b, s, hq, hkv, hd)
-        e1.record()
-        torch.cuda.synchronize()
-        t = e0.elapsed_time(e1) / 10 / 1e3
-        flops = 4 * b * s * s * hq * hd / 2
-        print(f"{name:20s} warps={os.environ.get('HX_PF_WARPS', '8')}: {t * 1e6:8.1f} us  {flops / t / 1e12:6.1f} TFLOP/s",
-              flush=True)
+        qkv = torch.randn(b * s, (hq + 2 * hkv) * hd, device="cuda").bfloat16()
+        vt = torch.empty(b * hkv * hd * s, device="cuda").bfloat16()
+        runs = {"mma.sync": lambda: ops.attn_prefill(q, kc, vc, bt, sl, o, b, s, hq, hkv, hd),
+                "tcgen05": lambda: ops.attn_prefill_tc(q, kc, vt, bt, o, b, s, hq, hkv, hd),
+                "tcgen05+vt": lambda: (ops.prefill_vt(qkv, vt, b, s, hq, hkv, hd),
+                                       ops.attn_prefill_tc(q, kc, vt, bt, o, b, s, hq, hkv, hd))}
+        for kind, fn in runs.items():
+            for _ in range(2):
+                fn()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(10):
+                fn()
+            e1.record()
+            torch.cuda.synchronize()
+            t = e0.elapsed_time(e1) / 10 / 1e3
+            flops = 4 * b * s * s * hq * hd / 2
+            print(f"{name:20s} {kind:11s}: {t * 1e6:8.1f} us  {flops / t / 1e12:6.1f} TFLOP/s", flush=True)
 
 
 if __name__ == "__main__":
