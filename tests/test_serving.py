@@ -1,0 +1,70 @@
+"""The measured service-time seam on CPU: the planner's
+simulator driven by a ``{(replica, TaskSpec): seconds}`` table -- the shape the
+engine's ``serve.measured_service_times`` returns -- reproduces the closed-form
+run exactly when the table holds the closed-form values, and the CLI's
+``simulate --service`` reads the JSON form of the same table."""
+
+import json
+import subprocess
+import sys
+from pathlib import Path
+
+from paper_2311_11514_b200 import planner as P
+from paper_2311_11514_b200.planner import cmdline
+
+ROOT = Path(__file__).resolve().parents[1]
+B = ROOT / "tests" / "golden" / "planner" / "b200_homog" / "inputs"
+
+
+def test_service_table_equals_cost_model_when_fed_its_values():
+    cluster, model = P.load_cluster(B / "cluster.json"), P.load_model(B / "model.json")
+    wl, slo = P.load_workload(B / "workload.json"), P.load_slo(B / "slo.json")
+    plan = P.load_plan(B / "plan.json")
+    reqs = P.generate_workload(wl)
+    table = P.service_times(plan, model, [r.task for r in reqs], cluster)
+    a = P.simulate(plan, reqs, slo, model, cluster)
+    b = P.simulate(plan, reqs, slo, model, cluster, service=dict(table))
+    assert a == b
+    # a slower measured replica shifts routing toward the others
+    slow = {k: (v * 3 if k[0] == 0 else v) for k, v in table.items()}
+    c = P.simulate(plan, reqs, slo, model, cluster, service=slow)
+    assert sum(o.replica == 0 for o in c.per_request) < sum(o.replica == 0 for o in a.per_request)
+
+
+def test_cli_simulate_with_service_file(tmp_path):
+    cluster, model = P.load_cluster(B / "cluster.json"), P.load_model(B / "model.json")
+    wl = P.load_workload(B / "workload.json")
+    plan = P.load_plan(B / "plan.json")
+    task = wl.dominant_task()
+    table = P.service_times(plan, model, [task], cluster)
+    doc = {"entries": [{"replica": r, "batch_size": t.batch_size, "input_len": t.input_len,
+                        "output_len": t.output_len, "seconds": s} for (r, t), s in table.items()]}
+    svc = tmp_path / "svc.json"
+    svc.write_text(json.dumps(doc))
+    common = ["simulate", "--cluster", str(B / "cluster.json"), "--model", str(B / "model.json"),
+              "--workload", str(B / "workload.json"), "--slo", str(B / "slo.json"), "--plan", str(B / "plan.json")]
+    assert cmdline.main(common + ["--out-dir", str(tmp_path / "a")]) == 0
+    assert cmdline.main(common + ["--out-dir", str(tmp_path / "b"), "--service", str(svc)]) == 0
+    for f in ("report.json", "requests.csv", "attainment_vs_scale.csv", "attainment_vs_rate.csv"):
+        assert (tmp_path / "a" / f).read_bytes() == (tmp_path / "b" / f).read_bytes(), f
+    # an incomplete table is an input error (exit 2), not a crash
+    doc["entries"] = doc["entries"][:1]
+    svc.write_text(json.dumps(doc))
+    assert cmdline.main(common + ["--out-dir", str(tmp_path / "c"), "--service", str(svc)]) == 2
+
+
+def test_c5_report_from_measured_entries(tmp_path):
+    svc = tmp_path / "svc"
+    svc.mkdir()
+    for i, (p, l, s) in enumerate([("[2,2]", [40, 40], 5.4), ("[2]", [80], 6.5), ("[4]", [80], 4.4)]):
+        (svc / f"p{i}.json").write_text(json.dumps({"plan": p, "layers": l, "seconds": s}))
+    out = tmp_path / "c5.json"
+    r = subprocess.run([sys.executable, str(ROOT / "tools" / "c5_report.py"), "--plan",
+                        str(ROOT / "tests/golden/planner/b200_422/plan_s0/plan.json"), "--svc", str(svc),
+                        "--out", str(out)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    d = json.loads(out.read_text())
+    ga = d["layouts"]["GA plan (b200 {4,2,2} buckets)"]
+    assert ga["pipelines"] == ["[2,2]", "[2]", "[2]"] and ga["service_s"] == [5.4, 6.5, 6.5]
+    assert all(0.0 <= a <= 1.0 for a in ga["attainment"])
+    assert "missing_measurement" in d["layouts"]["asymmetric 1 x [4,2,2] 40/20/20"]
