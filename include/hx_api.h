@@ -201,6 +201,13 @@ int hx_attn_prefill_tc(const void *q, const void *k_cache, const void *vt, const
                        void *o, int batch, int s_len, int hq, int hkv, int hd, int page_size,
                        int max_blocks, hx_stream_t stream);
 
+/* Consumer of a deferred gate/up GEMM (hx_linear with HX_LINEAR_DEFER_REDUCE
+ * into fp32 y [n_tok][ldy >= 2 inter], k_dim = its K): out (bf16) = silu(gate)
+ * * up with gate/up reduced from the split-K slots and rounded to bf16 --
+ * bit-identical to hx_linear (bf16 out) + hx_swiglu. */
+int hx_splitk_swiglu(const float *y, int ldy, const void *workspace, int n_tok, int inter,
+                     int k_dim, void *out, int ld_out, hx_stream_t stream);
+
 /* out[t, j] = silu(gu[t, j]) * gu[t, inter + j], j < inter */
 int hx_swiglu(const void *gu, void *out, int dtype, int n_tok, int inter,
               hx_stream_t stream);

@@ -782,6 +782,31 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// SwiGLU consumer of a deferred gate/up GEMM (fp32 y [n_tok][2 inter]): gate
+// and up gathered like the residual consumer (whole tiles from y, split tiles
+// from the partial slots in CTA order), rounded to bf16 exactly where the
+// in-kernel fix-up would have stored them, then silu(gate) * up as in
+// hx_swiglu -- identical bits, without the GEMM's fix-up tail.
+__global__ void __launch_bounds__(256)
+    sk_swiglu_kernel(const float *y, long ldy, SKView v, __nv_bfloat16 *out, long ld_out, int inter) {
+  pdl_trigger();
+  pdl_wait();
+  const int t = blockIdx.y;
+  const int f = (blockIdx.x * 256 + threadIdx.x) * 4;
+  if (f >= inter) return;
+  const float4 g = sk_gather4(v, y, ldy, t, f);
+  const float4 u = sk_gather4(v, y, ldy, t, f + inter);
+  const float gv[4] = {g.x, g.y, g.z, g.w}, uv[4] = {u.x, u.y, u.z, u.w};
+  float r[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float gb = __bfloat162float(__float2bfloat16_rn(gv[j]));
+    const float ub = __bfloat162float(__float2bfloat16_rn(uv[j]));
+    r[j] = (gb / (1.0f + expf(-gb))) * ub;
+  }
+  store4(out + (size_t)t * ld_out + f, r[0], r[1], r[2], r[3]);
+}
+
 // ------------------------------------------------------------------ packing
 // dst[(t * KB + kb) * 128 * 64 + r * 64 + c] = src[(t * 128 + r) * K + kb * 64 + c] (0 if OOB)
 __global__ void pack_weight_kernel(const __nv_bfloat16 *__restrict__ src, __nv_bfloat16 *__restrict__ dst,
@@ -1017,6 +1042,22 @@ extern "C" int hx_splitk_residual_rmsnorm(float *x, const float *y, int ldy, con
                           y, (long)ldy, v, gain, (__nv_bfloat16 *)out, n_out, eps);
   return launch_cluster(sk_residual_rmsnorm_kernel<float>, dim3(n_tok * SK_CL), dim3(256), 0, st, SK_CL, x, y,
                         (long)ldy, v, gain, (float *)out, n_out, eps);
+}
+
+extern "C" int hx_splitk_swiglu(const float *y, int ldy, const void *workspace, int n_tok, int inter, int k_dim,
+                                void *out, int ld_out, hx_stream_t stream) {
+  if (n_tok == 0) return 0;
+  if (!y || !workspace || !out || inter % 4 || ldy % 4 || ld_out % 4 || ldy < 2 * inter) return HX_ERR_ARG;
+  Plan pl = plan_gemm(n_tok, 2 * inter, k_dim);
+  if (!pl.decode) return HX_ERR_UNSUPPORTED;
+  SKView v;
+  v.ws = reinterpret_cast<const float *>(reinterpret_cast<const uint8_t *>(workspace) + kTicketBytes);
+  v.KB = (k_dim + BK - 1) / BK;
+  v.units = pl.tiles * v.KB;
+  v.G = sk_grid(v.units);
+  v.BN = pl.bn;
+  return launch(sk_swiglu_kernel, dim3((inter / 4 + 255) / 256, n_tok), dim3(256), 0, as_stream(stream), y, (long)ldy,
+                v, (__nv_bfloat16 *)out, (long)ld_out, inter);
 }
 
 extern "C" size_t hx_debug_trace(void *buf, size_t records) {

@@ -235,12 +235,23 @@ class RankExecutor:
         self.rope_tab = _ops.rope_table(self.max_ctx, self.hd, cfg.rope_theta, dev) if self.fuse_rope else None
         self.par = None          # ops.PeerAllReduce when TP>1 ranks run in separate processes
         self._peer_now = False
+        self._decode_now = False
         self.attn_ws = torch.zeros(max(self.attn_ws_bytes, 256) // 4 + 64, dtype=torch.int32, device=dev)
         # tcgen05 prefill attention (default; HX_PREFILL_TC=0 selects the mma.sync
         # kernel): needs V transposed per (sequence, kv head) -- a prefill-only scratch
         self.tc_prefill = (os.environ.get("HX_PREFILL_TC", "1") == "1" and dtype == torch.bfloat16
                            and dev.type == "cuda" and self.k is _ops and self.hd == 128 and page_size == 64)
         self.vt = z(batch * max_prompt * self.hkv * self.hd) if self.tc_prefill else None
+        # decode gate/up GEMM leaves split tiles as fp32 partials; the SwiGLU
+        # kernel reduces them (no fix-up tail in the GEMM). Worth it when the
+        # 128-row tiles are few enough that stream-K splits most of them
+        # (< 2 per SM): 7B -0.6%, 70B TP=4 -1.6%, 70B TP=1 (448 tiles) +0.5%.
+        # HX_DEFER_GU=0 / 1 forces it off / on.
+        env = os.environ.get("HX_DEFER_GU")
+        few_tiles = 2 * self.inter // 128 < 2 * 148
+        self.defer_gu = (dtype == torch.bfloat16 and dev.type == "cuda" and self.k is _ops and not self.fuse_swiglu
+                         and (env == "1" or (env is None and few_tiles)))
+        self.gu32 = z(batch, 2 * self.inter, dt=torch.float32) if self.defer_gu else None
         self._x_full = self.x
         self.bt, self.sl = self.kv.block_table, self.kv.seq_lens   # the current micro-batch's sequences
 
@@ -286,6 +297,7 @@ class RankExecutor:
         # TP=1 decode: the O/down GEMMs leave split tiles as partials and the
         # residual+norm kernel that consumes them does the reduction
         self._defer_now = self.defer and not prefill_len
+        self._decode_now = not prefill_len
         # TP>1 decode: the partial goes straight into this rank's NVLink-visible slot
         self._peer_now = self.par is not None and not prefill_len
         self._linear(lw["wo"], self.attn, self._partial_out(2 * li), n_tok)   # row-parallel partial
@@ -319,6 +331,9 @@ class RankExecutor:
         self._add_norm(self.hq * self.hd, lw["ln_mlp"], self.h, n_tok, 2 * li)
         if self.fuse_swiglu:  # gate/up GEMM with SwiGLU in its epilogue (weights interleaved)
             k.linear_swiglu(lw["wgu"], self.h, self.a, n_tok, self.lin_ws)
+        elif self.defer_gu and n_tok <= 64 and self._decode_now:
+            k.linear(lw["wgu"], self.h, self.gu32, n_tok, self.lin_ws, defer_reduce=True, **self._l2pf(0))
+            k.splitk_swiglu(self.gu32, self.lin_ws, n_tok, self.cfg.hidden_dim, self.a)
         else:
             k.linear(lw["wgu"], self.h, self.gu, n_tok, self.lin_ws, **self._l2pf(0))
             k.swiglu(self.gu, self.a, n_tok)

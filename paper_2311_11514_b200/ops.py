@@ -59,6 +59,7 @@ _SIGS = {
     "hx_handoff_pull": ([_P, _P, _SZ, _SZ, _P, _P], _I),
     "hx_prefill_vt": ([_P, _P, _I, _I, _I, _I, _I, _P], _I),
     "hx_attn_prefill_tc": ([_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P], _I),
+    "hx_splitk_swiglu": ([_P, _I, _P, _I, _I, _I, _P, _I, _P], _I),
     "hx_swiglu": ([_P, _P, _I, _I, _I, _P], _I),
     "hx_rope_kv_append": ([_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _F, _P], _I),
     "hx_attn_decode_paged": ([_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _SZ, _P], _I),
@@ -250,6 +251,13 @@ def interleave_gate_up(wgu: torch.Tensor, block: int = 64) -> torch.Tensor:
     g = wgu[:inter].reshape(inter // block, block, h)
     u = wgu[inter:].reshape(inter // block, block, h)
     return torch.stack([g, u], dim=1).reshape(two_i, h).contiguous()
+
+
+def splitk_swiglu(y, workspace, n_tok, k_dim, out):
+    """SwiGLU consuming a deferred gate/up GEMM (linear(..., defer_reduce=True) into fp32 y)."""
+    inter = out.shape[-1]
+    _check(load().hx_splitk_swiglu(_p(y), y.shape[-1], _p(workspace), n_tok, inter, k_dim, _p(out), out.shape[-1],
+                                   _stream()), "hx_splitk_swiglu")
 
 
 def swiglu(gu, out, n_tok):
