@@ -97,6 +97,25 @@ def test_pdl_off_gives_identical_bits():
     assert torch.equal(y1, y2)
 
 
+@pytest.mark.parametrize("n_tok,inter,k", [(8, 11008, 4096), (32, 7168, 8192), (3, 1408, 512), (32, 14336, 8192)])
+def test_deferred_gate_up_swiglu_bit_identical(n_tok, inter, k):
+    """linear(defer_reduce) into fp32 + splitk_swiglu == linear (bf16 gu) + swiglu, bitwise."""
+    w = ops.PackedWeight((torch.randn(2 * inter, k, device=DEV) * 0.02).bfloat16())
+    x = torch.randn(64, k, device=DEV).bfloat16()
+    ws = torch.zeros(ops.linear_workspace(torch.bfloat16, n_tok, 2 * inter, k) // 4 + 64, dtype=torch.int32,
+                     device=DEV)
+    gu = torch.empty(64, 2 * inter, device=DEV, dtype=torch.bfloat16)
+    a1 = torch.empty(64, inter, device=DEV, dtype=torch.bfloat16)
+    ops.linear(w, x, gu, n_tok, ws)
+    ops.swiglu(gu, a1, n_tok)
+    y = torch.zeros(64, 2 * inter, device=DEV)
+    a2 = torch.empty_like(a1)
+    ops.linear(w, x, y, n_tok, ws, defer_reduce=True)
+    ops.splitk_swiglu(y, ws, n_tok, k, a2)
+    torch.cuda.synchronize()
+    assert torch.equal(a1[:n_tok], a2[:n_tok])
+
+
 @pytest.mark.parametrize("n_tok,H,k", [(8, 4096, 4096), (8, 4096, 11008), (32, 8192, 2048), (3, 2048, 5632),
                                        (1, 256, 768)])
 def test_deferred_splitk_matches_in_kernel_reduction(n_tok, H, k):
