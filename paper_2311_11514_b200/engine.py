@@ -482,7 +482,6 @@ class Engine:
                               load_rank_weights(cfg, r, self.dtype, self.device, seed, weights),
                               kernels=self.kernels, page_size=page_size,
                               pack_weights=pack_weights and kernels is None) for r in local]
-        import os
         peer_allreduce = peer_allreduce and os.environ.get("HX_PEER_AR", "1") != "0"
         if (peer_allreduce and self.comm.kind == "dist" and self.device.type == "cuda" and kernels is None):
             for e in execs:

@@ -2,7 +2,6 @@
 
     python tools/attn_prefill_bench.py      # HX_PF_WARPS=4|8 selects the CTA shape
 """
-import os
 import sys
 from pathlib import Path
 
