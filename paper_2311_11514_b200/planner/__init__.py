@@ -29,10 +29,10 @@ from .evolution import (EvalOutcome, Genome, InfeasiblePoolError, SearchConfig, 
                         init_population, make_genome, mutate_merge, mutate_split, mutate_swap,
                         random_mutation_baseline, refine_partition, replan)
 from .grouping import cluster_groups, device_features, kmeans_fit
-from .layout_dp import DEFAULT_TP_CANDIDATES, DpResult, solve_pipeline, visited_state_count
+from .layout_dp import DEFAULT_TP_CANDIDATES, DpResult, DpTable, dp_transition, solve_pipeline, visited_state_count
 from .pool import (B200, Bucket, ClusterSpec, Device, GpuType, TypeVector, a100_like_cluster, b200_node,
-                   build_cluster, cluster_from_dict, cluster_to_dict, load_cluster, remove_devices,
-                   three_tier_cluster, two_region_cluster)
+                   build_cluster, cluster_from_dict, cluster_to_dict, llama70b, load_cluster, remove_devices,
+                   three_tier_cluster, toy_model, two_region_cluster)
 from .slo_sim import (SloConfig, SloReport, WorkloadSpec, generate_workload, load_slo, load_workload,
                       service_times, simulate, sweep_rate, sweep_slo_scale)
 

@@ -33,6 +33,51 @@ DEFAULT_TP_CANDIDATES = (1, 2, 4, 8)
 _NO_MOVE = (-1, -1)
 
 
+class DpTable:
+    """The DP memo as the reference exposes it (dp.py:42-95): best cost per
+    (stage index, assigned counts tau, entering move) with a parent link;
+    DP[0; 0] = 0, every other key +inf until relaxed, costs only decrease."""
+
+    def __init__(self, n_buckets: int):
+        self.n_buckets = n_buckets
+        self.entries: dict = {(0, (0,) * n_buckets, None): (0.0, None, ())}
+
+    def cost(self, key) -> float:
+        got = self.entries.get(key)
+        return got[0] if got else math.inf
+
+    def best_cost(self, stage_index: int, assigned) -> float:
+        """Minimum over the moves entering (j, tau)."""
+        assigned = tuple(assigned)
+        return min((c for (j, tau, _), (c, _, _) in self.entries.items() if j == stage_index and tau == assigned),
+                   default=math.inf)
+
+    def update(self, key, cost: float, parent, stage_devices=()) -> bool:
+        if cost < self.cost(key):
+            self.entries[key] = (cost, parent, tuple(stage_devices))
+            return True
+        return False
+
+
+def dp_transition(table: DpTable, stage_index: int, assigned, move, stage_cost: float) -> DpTable:
+    """One relaxation DP[j; tau] <- min(old, DP[j-1; tau - move] + stage_cost)
+    (dp.py:98-122); an infinite (memory-violating) stage cost changes nothing."""
+    k, n = move
+    assigned = tuple(assigned)
+    if n < 1 or not 0 <= k < len(assigned) or assigned[k] < n:
+        raise ValueError(f"move {move} exceeds assigned counts {assigned}")
+    prev = assigned[:k] + (assigned[k] - n,) + assigned[k + 1:]
+    base = table.best_cost(stage_index - 1, prev)
+    total = base + stage_cost if math.isfinite(base) and math.isfinite(stage_cost) else math.inf
+    if math.isfinite(total):
+        parent, pcost = None, math.inf
+        for key, (c, _, _) in table.entries.items():
+            if key[0] == stage_index - 1 and key[1] == prev and c < pcost:
+                parent, pcost = key, c
+        table.update((stage_index, assigned, tuple(move)), total, parent)
+    return table
+
+
 @dataclass
 class DpResult:
     cost: float

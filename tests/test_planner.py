@@ -254,3 +254,20 @@ def test_live_workload_and_search(H, seed):
     hr = Hg.random_mutation_baseline(hc, hm, hw, hs, hcfg)
     orr = P.random_mutation_baseline(oc, om, ow, os_, ocfg)
     assert [h.best_fitness for h in hr.history] == [h.best_fitness for h in orr.history]
+
+
+def test_dp_transition_table():
+    """dp.py:98-122 semantics (reference test_dp.py TestDpTransition)."""
+    import math as _m
+    t = P.DpTable(2)
+    P.dp_transition(t, 1, (1, 0), (0, 1), 1.5)
+    assert t.best_cost(1, (1, 0)) == 1.5
+    P.dp_transition(t, 1, (1, 0), (0, 1), 2.0)
+    assert t.best_cost(1, (1, 0)) == 1.5
+    t2 = P.DpTable(2)
+    P.dp_transition(t2, 1, (1, 0), (0, 1), _m.inf)
+    assert _m.isinf(t2.best_cost(1, (1, 0)))
+    with pytest.raises(ValueError):
+        P.dp_transition(t2, 1, (1, 0), (0, 2), 1.0)
+    assert P.llama70b().param_bytes() == 12 * 8192 * 8192 * 2 * 80
+    assert P.toy_model().num_layers == 8
