@@ -399,6 +399,7 @@ def main():
                        "parallelism": "pp%d-tp[%s]" % (len(w["tps"]), ",".join(map(str, w["tps"]))),
                        "l2": "weights stream from HBM each step (>> 126 MB L2); no flush"},
             "p50_decode_step_ms": round(p50, 4) if p50 else None,
+            "p90_decode_step_ms": round(float(np.percentile(steps_ms, 90)), 4) if steps_ms else None,
             "prefill_ms": round(pre_s / args.steps * 1e3, 3),
             "decode_ms_per_request": round(dec_s / args.steps * 1e3, 3),
             "decode_s_all_ranks": round(dec_all / args.steps, 4),
