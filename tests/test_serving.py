@@ -68,3 +68,35 @@ def test_c5_report_from_measured_entries(tmp_path):
     assert ga["pipelines"] == ["[2,2]", "[2]", "[2]"] and ga["service_s"] == [5.4, 6.5, 6.5]
     assert all(0.0 <= a <= 1.0 for a in ga["attainment"])
     assert "missing_measurement" in d["layouts"]["asymmetric 1 x [4,2,2] 40/20/20"]
+
+
+def test_plan_with_measured_service_model(tmp_path):
+    """plan --service: measurements equal to the closed form (scale 1) give the
+    byte-identical reference plan; the B200 measurements of profiles/r01/c5
+    drive the GA to a valid plan."""
+    B4 = ROOT / "tests" / "golden" / "planner" / "b200_422" / "inputs"
+    cluster, model = P.load_cluster(B4 / "cluster.json"), P.load_model(B4 / "model.json")
+    task = P.load_workload(B4 / "workload.json").dominant_task()
+    meas = tmp_path / "meas"
+    meas.mkdir()
+    for i, (tps, layers) in enumerate((((2, 2), (40, 40)), ((2,), (80,)), ((4,), (80,)))):
+        pipe = cmdline._place_shape(tuple(zip(tps, layers)), cluster)
+        secs = P.pipeline_cost(pipe, model, task, cluster)[0]
+        (meas / f"p{i}.json").write_text(json.dumps({
+            "plan": "[" + ",".join(map(str, tps)) + "]", "layers": list(layers), "seconds": secs,
+            "batch_size": task.batch_size, "input_len": task.input_len, "output_len": task.output_len}))
+    common = ["plan", "--cluster", str(B4 / "cluster.json"), "--model", str(B4 / "model.json"),
+              "--workload", str(B4 / "workload.json"), "--slo", str(B4 / "slo.json"),
+              "--pop", "16", "--gens", "30", "--seed", "0"]
+    assert cmdline.main(common + ["--out-dir", str(tmp_path / "a"), "--service", str(meas)]) == 0
+    gold = ROOT / "tests" / "golden" / "planner" / "b200_422" / "plan_s0" / "plan.json"
+    assert (tmp_path / "a" / "plan.json").read_bytes() == gold.read_bytes()
+    real = ROOT / "profiles" / "r01" / "c5"
+    svc_dir = tmp_path / "real"
+    svc_dir.mkdir()
+    for f in real.glob("p[0-9]*.json"):
+        (svc_dir / f.name).write_text(f.read_text())
+    assert cmdline.main(common + ["--out-dir", str(tmp_path / "b"), "--service", str(svc_dir)]) == 0
+    plan = P.load_plan(tmp_path / "b" / "plan.json")
+    assert sorted(d for pipe in plan.pipelines for st in pipe for d in st.devices) == sorted(
+        set(d for pipe in plan.pipelines for st in pipe for d in st.devices))
