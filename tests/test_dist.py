@@ -36,7 +36,7 @@ def _run(nproc, args, timeout=600, **extra_env):
     return r.stdout
 
 
-@pytest.mark.parametrize("plan,layers", [("2,1", "3,1"), ("1,2", "1,3"), ("1,1", "2,2")])
+@pytest.mark.parametrize("plan,layers", [("2,1", "3,1"), ("1,2", "1,3"), ("1,1", "2,2"), ("4,2,2", "2,1,1")])
 def test_gloo_asymmetric_plans(plan, layers):
     n = sum(int(x) for x in plan.split(","))
     _run(n, ["--plan", plan, "--layers", layers, "--cpu"])
