@@ -241,3 +241,35 @@ def bf16_weights(w: dict) -> dict:
     out["layers"] = {l: {k: (v if k.startswith("ln_") else bf16_round(v)) for k, v in lw.items()}
                      for l, lw in w["layers"].items()}
     return out
+
+
+def streamed_teacher_forced(cfg, seed, seq, positions, modes=((True, True), (True, False))):
+    """Teacher-forced logits of a full-depth model without holding it in host
+    RAM (C2: 7B fp32 is 27 GB): one causal pass over ``seq`` [b, t] (prompt +
+    forced tokens), layer by layer, each layer's weights drawn from the same
+    seeded streams as ``init_tensor`` (``weights.layer_stream``), used by every
+    mode and dropped. Equivalent to prefill + teacher-forced decode steps (the
+    layer math is per position except the causal attention; the engine stores
+    bf16 at the same points in both phases when the GEMM epilogues are
+    unfused). ``modes``: (weights rounded to bf16, activations rounded to bf16)
+    pairs; returns {mode: logits [len(positions), b, V]}."""
+    from paper_2311_11514_b200.weights import init_globals, layer_stream
+    seq = np.asarray(seq)
+    modes = [tuple(m) for m in modes]
+    g32 = init_globals(cfg, seed, ("embed", "norm", "lm_head"))
+    gb = {k: (v if k == "norm" else bf16_round(v)) for k, v in g32.items()}
+    glob = {True: gb, False: g32}
+    xs = {m: glob[m[0]]["embed"][seq].astype(F32) for m in modes}
+    for l, lw in layer_stream(cfg, seed, range(cfg.num_layers)):
+        w = {False: {"layers": {l: lw}}}
+        if any(m[0] for m in modes):
+            w[True] = {"layers": {l: {k: (v if k.startswith("ln_") else bf16_round(v)) for k, v in lw.items()}}}
+        for m in modes:
+            xs[m] = Oracle(cfg, w[m[0]], act_bf16=m[1], fused=(False, False)).layer(l, xs[m], 0, Cache())
+        del w, lw
+    pos = list(positions)
+    out = {}
+    for m in modes:
+        o = Oracle(cfg, glob[m[0]], act_bf16=m[1], fused=(False, False))
+        out[m] = np.stack([o.logits(xs[m][:, p]) for p in pos], 0)
+    return out

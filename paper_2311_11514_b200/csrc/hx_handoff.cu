@@ -133,6 +133,13 @@ extern "C" size_t hx_handoff_inbox_bytes(size_t max_words) { return 3 * max_word
 
 extern "C" int hx_handoff_inbox_init(void *inbox, size_t max_words, hx_stream_t stream) {
   if (!inbox || !max_words || max_words % 4) return HX_ERR_ARG;
+  // Load both ends of the protocol now: under CUDA lazy loading the first launch
+  // of a kernel loads its module, which cannot complete while a spinning pull
+  // occupies the device -- a pull launched before the push's first-ever launch in
+  // the same context (single-GPU emulation) would then never see its data.
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, handoff_push_kernel);
+  cudaFuncGetAttributes(&fa, handoff_pull_kernel);
   handoff_fill_kernel<<<148, 256, 0, as_stream(stream)>>>((uint32_t *)inbox, 3 * max_words);
   return launch_status();
 }

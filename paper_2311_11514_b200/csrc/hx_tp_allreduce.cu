@@ -312,6 +312,10 @@ extern "C" size_t hx_tp_inbox_bytes(int tp, int max_tok, int hidden) {
 
 extern "C" int hx_tp_inbox_init(void *inbox, int tp, int max_tok, int hidden, hx_stream_t stream) {
   if (!inbox || tp < 1 || max_tok < 1 || hidden < 1) return HX_ERR_ARG;
+  // load the kernel before any rank spins in it (lazy loading, see hx_handoff_inbox_init)
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, tp_ar_push_rmsnorm_kernel<float>);
+  cudaFuncGetAttributes(&fa, tp_ar_push_rmsnorm_kernel<__nv_bfloat16>);
   const size_t n = hx_tp_inbox_bytes(tp, max_tok, hidden) / 4;
   fill_u32_kernel<<<296, 256, 0, as_stream(stream)>>>((uint32_t *)inbox, n, kSentinel);
   return launch_status();

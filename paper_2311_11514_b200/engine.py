@@ -38,7 +38,7 @@ from .comm import make_comm
 from .config import LlamaConfig
 from .plan import GlobalAssignment, InputError, TaskSpec
 from .topology import Role, pipeline_roles, role_of
-from .weights import _CODES, LAYER_TENSORS, init_tensor, shard_layer, tensor_shape
+from .weights import _CODES, LAYER_TENSORS, init_globals, layer_stream, shard_layer, tensor_shape
 
 DTYPES = {"bf16": torch.bfloat16, "fp32": torch.float32}
 
@@ -80,33 +80,48 @@ def _shard_device(cfg, lw, r, tp):
 
 def load_rank_weights(cfg: LlamaConfig, role: Role, dtype: torch.dtype, device, seed: int = 0,
                       source: str = "host") -> dict:
-    """Weight shards for one role. ``source='host'`` draws the bit-exact
-    numpy stream the CPU oracle uses; ``'device'`` generates on the GPU (same
-    distribution, different bits) for throughput runs of large models."""
-    r, tp = role.tp_rank, role.tp
-    out = {"layers": []}
+    """Weight shards for one role (see ``load_weights``)."""
+    return load_weights(cfg, [role], dtype, device, seed, source)[role.device]
+
+
+def load_weights(cfg: LlamaConfig, roles, dtype: torch.dtype, device, seed: int = 0,
+                 source: str = "host") -> dict:
+    """Weight shards for the given roles, ``{role.device: shards}``. Each layer
+    is drawn once and sharded for every local TP rank that owns it.
+    ``source='host'`` draws the bit-exact numpy streams the CPU oracle uses
+    (threaded, ``weights.layer_stream``); ``'device'`` generates on the GPU
+    (same distribution, different bits) for throughput runs of large models."""
+    out = {r.device: {"layers": []} for r in roles}
 
     def put(x, keep_fp32=False):
         t = torch.as_tensor(x) if isinstance(x, np.ndarray) else x
         return t.to(device=device, dtype=torch.float32 if keep_fp32 else dtype).contiguous()
 
-    for l in range(*role.layers):
-        if source == "host":
-            lw = {n: init_tensor(cfg, seed, n, l) for n in LAYER_TENSORS}
-            sh = shard_layer(cfg, lw, r, tp)
-        else:
-            lw = {n: _device_tensor(cfg, seed, n, l, device) for n in LAYER_TENSORS}
-            sh = _shard_device(cfg, lw, r, tp)
-        out["layers"].append({k: put(v, keep_fp32=k.startswith("ln_")) for k, v in sh.items()})
-        del lw, sh
-    gen = (lambda n: init_tensor(cfg, seed, n)) if source == "host" else \
-        (lambda n: _device_tensor(cfg, seed, n, -1, device))
-    if role.is_first:
-        out["embed"] = put(gen("embed"))
-    if role.is_last:
-        out["norm"] = put(gen("norm"), keep_fp32=True)
-        vr = cfg.vocab // tp
-        out["lm_head"] = put(gen("lm_head")[r * vr:(r + 1) * vr])
+    owners = {}
+    for r in roles:
+        for l in range(*r.layers):
+            owners.setdefault(l, []).append(r)
+    layers = sorted(owners)
+    if source == "host":
+        stream = layer_stream(cfg, seed, layers)
+    else:
+        stream = ((l, {n: _device_tensor(cfg, seed, n, l, device) for n in LAYER_TENSORS}) for l in layers)
+    for l, lw in stream:
+        for r in owners[l]:
+            sh = shard_layer(cfg, lw, r.tp_rank, r.tp) if source == "host" else _shard_device(cfg, lw, r.tp_rank, r.tp)
+            out[r.device]["layers"].append({k: put(v, keep_fp32=k.startswith("ln_")) for k, v in sh.items()})
+            del sh
+        del lw
+    want = sorted({n for r in roles for n in (["embed"] if r.is_first else []) + (["norm", "lm_head"] if r.is_last else [])})
+    glob = init_globals(cfg, seed, want) if source == "host" else \
+        {n: _device_tensor(cfg, seed, n, -1, device) for n in want}
+    for r in roles:
+        if r.is_first:
+            out[r.device]["embed"] = put(glob["embed"])
+        if r.is_last:
+            out[r.device]["norm"] = put(glob["norm"], keep_fp32=True)
+            vr = cfg.vocab // r.tp
+            out[r.device]["lm_head"] = put(glob["lm_head"][r.tp_rank * vr:(r.tp_rank + 1) * vr])
     return out
 
 
@@ -234,6 +249,7 @@ class RankExecutor:
         self._defer_now = False
         self.rope_tab = _ops.rope_table(self.max_ctx, self.hd, cfg.rope_theta, dev) if self.fuse_rope else None
         self.par = None          # ops.PeerAllReduce when TP>1 ranks run in separate processes
+        self.stream = None       # this emulated rank's stream (Engine(local_peer=True))
         self._peer_now = False
         self._decode_now = False
         self.attn_ws = torch.zeros(max(self.attn_ws_bytes, 256) // 4 + 64, dtype=torch.int32, device=dev)
@@ -326,9 +342,16 @@ class RankExecutor:
         else:                   # proj already all-reduced (NCCL) or TP=1 prefill
             self.k.residual_add_rmsnorm(self.x, self.proj, gain, out, n_tok, self.cfg.rms_eps)
 
+    def mlp_norm(self, li: int, n_tok: int):
+        """all-reduce #1 (TP>1 decode: fused into this kernel) + residual + RMSNorm."""
+        self._add_norm(self.hq * self.hd, self.w["layers"][li]["ln_mlp"], self.h, n_tok, 2 * li)
+
     def mlp_block(self, li: int, n_tok: int):
+        self.mlp_norm(li, n_tok)
+        self.mlp_body(li, n_tok)
+
+    def mlp_body(self, li: int, n_tok: int):
         k, lw = self.k, self.w["layers"][li]
-        self._add_norm(self.hq * self.hd, lw["ln_mlp"], self.h, n_tok, 2 * li)
         if self.fuse_swiglu:  # gate/up GEMM with SwiGLU in its epilogue (weights interleaved)
             k.linear_swiglu(lw["wgu"], self.h, self.a, n_tok, self.lin_ws)
         elif self.defer_gu and n_tok <= 64 and self._decode_now:
@@ -359,77 +382,164 @@ class RankExecutor:
 
 
 # --------------------------------------------------------------------- driver
+class RankStreams:
+    """Single-GPU emulation of a multi-GPU decode step with the REAL collective
+    kernels (``Engine(..., local_peer=True)``): every emulated rank launches on
+    its own CUDA stream and the peer pointers of the NVLink all-reduce and the
+    P2P hand-offs are same-device pointers.
+
+    * Work between collectives is serialised across ranks with events, so two
+      ranks' persistent GEMMs never compete for the SMs.
+    * The all-reduce kernels of a stage wait for the whole chain and are then
+      launched on all of its ranks' streams at once: they run concurrently and
+      genuinely wait for each other's pushes (the protocol of the multi-GPU
+      path; ``tp * n_tok * 4`` CTAs must be co-resident, checked by the engine).
+    * A hand-off pull is ordered after its push (no long spin on one GPU).
+    Outside ``begin()`` / ``end()`` (the prefill) everything runs on the
+    caller's stream."""
+
+    def __init__(self, execs, device):
+        for e in execs:
+            e.stream = torch.cuda.Stream(device)
+        self.active = False
+        self.deps = []
+
+    def _event(self, stream):
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        self.last[stream] = ev
+        return ev
+
+    def begin(self):
+        self.main = torch.cuda.current_stream()
+        self.last = {}
+        self.deps = [self._event(self.main)]
+        self.active = True
+
+    def end(self):
+        # join every rank stream's last work (a graph capture needs every fork joined)
+        for st, ev in self.last.items():
+            if st != self.main:
+                self.main.wait_event(ev)
+        self.deps, self.active, self.last = [], False, {}
+
+    def serial(self, execs, fn):
+        if not self.active:
+            for e in execs:
+                fn(e)
+            return
+        for e in execs:
+            for ev in self.deps:
+                e.stream.wait_event(ev)
+            with torch.cuda.stream(e.stream):
+                fn(e)
+            self.deps = [self._event(e.stream)]
+
+    def concurrent(self, execs, fn):
+        if not self.active:
+            for e in execs:
+                fn(e)
+            return
+        for e in execs:
+            for ev in self.deps:
+                e.stream.wait_event(ev)
+        evs = []
+        for e in execs:
+            with torch.cuda.stream(e.stream):
+                fn(e)
+            evs.append(self._event(e.stream))
+        self.deps = evs
+
+
 class StageDriver:
     """Runs the TP ranks of one stage (all of them when emulated in one
     process, or the single local one under torch.distributed)."""
 
-    def __init__(self, execs: list[RankExecutor], comm, stage: int):
+    def __init__(self, execs: list[RankExecutor], comm, stage: int, sched: RankStreams | None = None):
         self.execs, self.comm, self.stage = execs, comm, stage
         self.role = execs[0].role
         self.tp = self.role.tp
+        self.sched = sched
+
+    def _each(self, fn):
+        """fn(e) for every local rank (serialised across emulated rank streams)."""
+        if self.sched is None:
+            for e in self.execs:
+                fn(e)
+        else:
+            self.sched.serial(self.execs, fn)
+
+    def _together(self, fn):
+        """fn(e) for every local rank; under RankStreams launched concurrently (collectives)."""
+        if self.sched is None:
+            for e in self.execs:
+                fn(e)
+        else:
+            self.sched.concurrent(self.execs, fn)
 
     def _ar(self, n_tok):
         if self.tp > 1 and not self.execs[0]._peer_now:  # peer path reduces inside the next kernel
             self.comm.all_reduce_sum([e.proj[:n_tok] for e in self.execs], self.role.tp_group)
 
     def embed(self, n_tok: int, prefill: bool):
-        for e in self.execs:
-            src = e.prompt if prefill else e.ids
-            e.k.embed(src, e.w["embed"], e.x, n_tok)
+        self._each(lambda e: e.k.embed(e.prompt if prefill else e.ids, e.w["embed"], e.x, n_tok))
 
     def layers(self, n_tok: int, prefill_len: int):
         for li in range(self.execs[0].n_layers):
-            for e in self.execs:
-                e.attn_block(li, n_tok, prefill_len)
+            self._each(lambda e: e.attn_block(li, n_tok, prefill_len))
             self._ar(n_tok)
-            for e in self.execs:
-                e.mlp_block(li, n_tok)
+            self._together(lambda e: e.mlp_norm(li, n_tok))
+            self._each(lambda e: e.mlp_body(li, n_tok))
             self._ar(n_tok)
-            for e in self.execs:
-                e.post_block(li, n_tok)
+            self._together(lambda e: e.post_block(li, n_tok))
         adv = prefill_len if prefill_len else 1
-        for e in self.execs:
-            e.k.advance(e.sl, e.sl.numel(), adv)
+        self._each(lambda e: e.k.advance(e.sl, e.sl.numel(), adv))
 
     def head(self, prefill_len: int):
-        for e in self.execs:
-            e.head(prefill_len)
+        self._each(lambda e: e.head(prefill_len))
         if self.tp > 1:
-            self.comm.all_reduce_max([e.keys for e in self.execs], self.role.tp_group)
-        for e in self.execs:
-            e.finalize()
+            keys = [e.keys for e in self.execs]
+            if self.sched is None:
+                self.comm.all_reduce_max(keys, self.role.tp_group)
+            else:
+                self.sched.serial(self.execs[-1:], lambda e: self.comm.all_reduce_max(keys, self.role.tp_group))
+        self._each(lambda e: e.finalize())
 
     def send_hidden(self, n_tok, decode: bool = False):
-        for e in self.execs:
+        def one(e):
             if decode and e.p2p_send:      # NVLink P2P store into each receiver's inbox
                 for link in e.p2p_send:
                     link.push(e.x[:n_tok])
-                continue
+                return
             for dst in e.role.send_to:
                 self.comm.send(e.x[:n_tok], e.role.device, dst)
+        self._each(one)
 
     def recv_hidden(self, n_tok, decode: bool = False):
-        for e in self.execs:
+        def one(e):
             if decode and e.p2p_recv is not None:
                 e.p2p_recv.pull(e.x[:n_tok])
-                continue
+                return
             self.comm.recv(e.x[:n_tok], e.role.recv_from, e.role.device)
+        self._each(one)
 
     def send_ids(self):
-        for e in self.execs:
+        def one(e):
             if e.ids_send:
                 for link in e.ids_send:
                     link.push(e.ids)
-                continue
+                return
             for dst in e.role.ids_send_to:
                 self.comm.send(e.ids, e.role.device, dst)
+        self._each(one)
 
     def recv_ids(self):
-        for e in self.execs:
+        def one(e):
             if e.ids_recv is not None:
                 e.ids_recv.pull(e.ids)
-                continue
+                return
             self.comm.recv(e.ids, e.role.ids_recv_from, e.role.device)
+        self._each(one)
 
 
 # --------------------------------------------------------------------- engine
@@ -455,7 +565,7 @@ class Engine:
                  batch: int, max_prompt: int, max_out: int, pipeline: int = 0, comm: str = "local",
                  device=None, seed: int = 0, weights: str = "host", page_size: int = 64,
                  use_graphs: bool = True, kernels=None, pack_weights: bool = True,
-                 peer_allreduce: bool = True):
+                 peer_allreduce: bool = True, local_peer: bool | None = None):
         if dtype not in DTYPES:
             raise InputError(f"dtype must be one of {sorted(DTYPES)}")
         self.plan, self.cfg, self.dtype = plan, cfg, DTYPES[dtype]
@@ -478,25 +588,44 @@ class Engine:
         self.kernels = kernels or _ops
         if self.device.type == "cuda":
             _ops.load()
-        execs = [RankExecutor(cfg, r, self.dtype, batch, max_prompt, max_out, self.device,
-                              load_rank_weights(cfg, r, self.dtype, self.device, seed, weights),
+        shards = load_weights(cfg, local, self.dtype, self.device, seed, weights)
+        execs = [RankExecutor(cfg, r, self.dtype, batch, max_prompt, max_out, self.device, shards.pop(r.device),
                               kernels=self.kernels, page_size=page_size,
                               pack_weights=pack_weights and kernels is None) for r in local]
         peer_allreduce = peer_allreduce and os.environ.get("HX_PEER_AR", "1") != "0"
-        if (peer_allreduce and self.comm.kind == "dist" and self.device.type == "cuda" and kernels is None):
+        native = self.device.type == "cuda" and kernels is None
+        # single-GPU emulation that still runs the multi-GPU collective kernels
+        # (NVLink all-reduce, P2P hand-offs) -- one stream per emulated rank
+        if local_peer is None:
+            local_peer = os.environ.get("HX_LOCAL_PEER", "0") == "1"
+        self.local_peer = bool(local_peer and self.comm.kind == "local" and native and peer_allreduce)
+        if self.local_peer:
+            worst = max(r.tp for r in roles) * batch * 4
+            if worst > 148 * 4:
+                raise InputError(f"local_peer emulation needs tp*batch*4 <= {148 * 4} co-resident all-reduce "
+                                 f"CTAs (got {worst})")
+        if peer_allreduce and self.comm.kind == "dist" and native:
             for e in execs:
                 if e.role.tp > 1:  # fused NVLink all-reduce for the decode step
                     e.par = _ops.PeerAllReduce(e.role.tp_rank, e.role.tp, batch, cfg.hidden_dim, 2 * e.n_layers,
                                                self.comm.groups[e.role.tp_group], self.comm.dist)
+        elif self.local_peer:
+            for j in sorted({r.stage for r in roles}):
+                st = sorted((e for e in execs if e.role.stage == j), key=lambda e: e.role.tp_rank)
+                if st[0].role.tp > 1:
+                    for e, par in zip(st, _ops.PeerAllReduce.local_group(st[0].role.tp, batch, cfg.hidden_dim,
+                                                                         2 * st[0].n_layers)):
+                        e.par = par
         for e in execs:
             e.p2p_send, e.p2p_recv, e.ids_send, e.ids_recv = [], None, [], None
-        self._p2p = (self.comm.kind == "dist" and self.device.type == "cuda" and kernels is None
+        self._p2p = ((self.comm.kind == "dist" or self.local_peer) and native
                      and self.num_stages > 1 and os.environ.get("HX_P2P", "1") != "0")
         if self._p2p:
             self._setup_p2p(execs)
+        self.sched = RankStreams(execs, self.device) if self.local_peer else None
         self.drivers = []
         for j in sorted({r.stage for r in local}):
-            self.drivers.append(StageDriver([e for e in execs if e.role.stage == j], self.comm, j))
+            self.drivers.append(StageDriver([e for e in execs if e.role.stage == j], self.comm, j, self.sched))
         self.execs = execs
         self.use_graphs = use_graphs and self.device.type == "cuda"
         self._graphs = None
@@ -514,22 +643,27 @@ class Engine:
             links += [("ids", r.device, dst) for dst in r.ids_send_to]
         mine = {e.role.device: e for e in execs}
         for kind, src, dst in sorted(links):
-            me = src if src in mine else dst if dst in mine else None
-            if me is None:
-                continue
             words = self.batch * (self.cfg.hidden_dim if kind == "hidden" else 1)
-            link = _ops.P2PLink(src, dst, me, words, self.comm.pairs[(min(src, dst), max(src, dst))],
-                                self.comm.dist)
-            e = mine[me]
-            if kind == "hidden":
-                if me == src:
-                    e.p2p_send.append(link)
-                else:
-                    e.p2p_recv = link
-            elif me == src:
-                e.ids_send.append(link)
+            if self.local_peer:           # both ends in this process
+                link = _ops.P2PLink.local(src, dst, words)
+                ends = [(mine[src], True), (mine[dst], False)]
             else:
-                e.ids_recv = link
+                me = src if src in mine else dst if dst in mine else None
+                if me is None:
+                    continue
+                link = _ops.P2PLink(src, dst, me, words, self.comm.pairs[(min(src, dst), max(src, dst))],
+                                    self.comm.dist)
+                ends = [(mine[me], me == src)]
+            for e, sender in ends:
+                if kind == "hidden":
+                    if sender:
+                        e.p2p_send.append(link)
+                    else:
+                        e.p2p_recv = link
+                elif sender:
+                    e.ids_send.append(link)
+                else:
+                    e.ids_recv = link
 
     # ---------------------------------------------------------------- steps
     def prefill_microbatches(self, b: int, s: int) -> int:
@@ -602,7 +736,30 @@ class Engine:
         if d.stage < self.num_stages - 1:
             d.send_hidden(b, decode=True)
 
+    def _decode_emulated_peer(self, b):
+        """The whole pipeline's decode step on one GPU with the multi-GPU
+        collective kernels (RankStreams): token ids back to stage 0 over the P2P
+        link, then stage by stage with NVLink-style all-reduces and hand-offs."""
+        self.sched.begin()
+        if self.num_stages > 1:
+            self.drivers[-1].send_ids()
+            self.drivers[0].recv_ids()
+        for d in self.drivers:
+            if d.stage > 0:
+                d.recv_hidden(b, decode=True)
+            self._decode_compute(d, b)
+            if d.stage < self.num_stages - 1:
+                d.send_hidden(b, decode=True)
+        self.sched.end()
+
     def _decode_step(self, b, graphs=None):
+        if self.local_peer:
+            if graphs is not None:
+                graphs[0].replay()
+                self._replayed += self._graph_launches[0]
+            else:
+                self._decode_emulated_peer(b)
+            return
         if self._p2p:
             for i, d in enumerate(self.drivers):
                 if graphs is not None:
@@ -630,6 +787,13 @@ class Engine:
         if self._graphs is not None and self._graph_key == key:
             return self._graphs
         graphs, counts = [], []
+        if self.local_peer:   # one graph over every emulated rank's stream (fork / join by events)
+            g = torch.cuda.CUDAGraph()
+            n0 = self._launch_count()
+            with torch.cuda.graph(g, capture_error_mode="thread_local"):
+                self._decode_emulated_peer(b)
+            self._graphs, self._graph_key, self._graph_launches = [g], key, [self._launch_count() - n0]
+            return self._graphs
         for d in self.drivers:
             g = torch.cuda.CUDAGraph()
             n0 = self._launch_count()

@@ -345,62 +345,96 @@ def kv_bytes(dtype, layers, num_blocks, hkv_rank, page, hd) -> int:
 
 
 # ---------------------------------------------------------------- NVLink TP all-reduce
+def _alloc(nbytes: int) -> int:
+    p = ctypes.c_void_p()
+    _check(load().hx_ipc_alloc(ctypes.byref(p), nbytes), "hx_ipc_alloc")
+    return p.value
+
+
 class PeerAllReduce:
     """Per-rank state of the fused NVLink all-reduce + residual + RMSNorm of a
-    TP>1 decode step, in cudaIpc-exported memory mapped on every rank of the TP
-    group (handles exchanged once over ``group``):
+    TP>1 decode step. Buffers are cudaIpc-exportable allocations mapped on every
+    rank of the TP group (handles exchanged once over ``group``):
 
     * ``mode='push'`` (default, hx_tp_allreduce_push_residual_rmsnorm): each
       rank stores its partial into every peer's sentinel-armed inbox and polls
       its own -- one one-way NVLink trip per call;
     * ``mode='pull'`` (hx_tp_allreduce_residual_rmsnorm): epoch flags, then
       peer loads of every rank's partial slot.
-    Both sum in rank order and give identical bits."""
+    Both sum in rank order and give identical bits.
+
+    ``PeerAllReduce.local_group`` builds all TP ranks of a group inside one
+    process on one device (peer pointers are plain same-device pointers): the
+    same kernels, each emulated rank launching on its own stream, so the
+    protocol runs with real concurrency on a single GPU."""
 
     def __init__(self, rank: int, tp: int, max_tok: int, hidden: int, sites: int, group, dist, mode: str | None = None):
-        import os
-        lib = load()
-        self.mode = mode or os.environ.get("HX_AR_MODE", "push")
-        if self.mode not in ("push", "pull"):
-            raise HxError(f"unknown all-reduce mode {self.mode!r}")
-        self.rank, self.tp, self.max_tok, self.hidden, self.sites = rank, tp, max_tok, hidden, sites
-        slot_bytes = max_tok * hidden * 4
-        bufs = [("slot0", slot_bytes), ("slot1", slot_bytes)]
-        if self.mode == "pull":
-            bufs.append(("flags", sites * max_tok * 8 * 4))
-        else:
-            bufs.append(("inbox", int(lib.hx_tp_inbox_bytes(tp, max_tok, hidden))))
-        self._own = []
-        ptrs = {}
-        for name, nbytes in bufs:
-            p = ctypes.c_void_p()
-            _check(lib.hx_ipc_alloc(ctypes.byref(p), nbytes), "hx_ipc_alloc")
-            self._own.append(p.value)
-            ptrs[name] = p.value
-        if self.mode == "push":
-            _check(lib.hx_tp_inbox_init(ptrs["inbox"], tp, max_tok, hidden, None), "hx_tp_inbox_init")
-            torch.cuda.synchronize()
+        self._setup(rank, tp, max_tok, hidden, sites, mode)
+        ptrs = self._alloc_own()
         handles = {}
+        lib = load()
         for name, p in ptrs.items():
             h = ctypes.create_string_buffer(64)
             _check(lib.hx_ipc_handle(p, h), "hx_ipc_handle")
             handles[name] = h.raw
         gathered = [None] * tp
         dist.all_gather_object(gathered, handles, group=group)
-        self._opened = []
-        self.peer = {name: [0] * tp for name in ptrs}
+        peer = {name: [0] * tp for name in ptrs}
         for r in range(tp):
             for name in ptrs:
                 if r == rank:
-                    self.peer[name][r] = ptrs[name]
+                    peer[name][r] = ptrs[name]
                 elif name in ("flags", "inbox") or self.mode == "pull":
                     q = ctypes.c_void_p()
                     _check(lib.hx_ipc_open(gathered[r][name], ctypes.byref(q)), "hx_ipc_open")
-                    self.peer[name][r] = q.value
+                    peer[name][r] = q.value
                     self._opened.append(q.value)
-        self.site_state = torch.zeros(2 * sites, dtype=torch.int32, device="cuda")
-        self._arr = {name: (ctypes.c_void_p * tp)(*self.peer[name]) for name in ptrs}
+        self._finish(peer)
+        self._group, self._dist = group, dist
         dist.barrier(group=group)
+
+    @classmethod
+    def local_group(cls, tp: int, max_tok: int, hidden: int, sites: int, mode: str | None = None):
+        """All ``tp`` ranks of one group in this process (single-GPU emulation)."""
+        objs = [cls.__new__(cls) for _ in range(tp)]
+        own = []
+        for r, o in enumerate(objs):
+            o._setup(r, tp, max_tok, hidden, sites, mode)
+            o._group = o._dist = None
+            own.append(o._alloc_own())
+        for r, o in enumerate(objs):
+            o._finish({name: [own[q][name] for q in range(tp)] for name in own[r]})
+        torch.cuda.synchronize()
+        return objs
+
+    def _setup(self, rank, tp, max_tok, hidden, sites, mode):
+        self.mode = mode or os.environ.get("HX_AR_MODE", "push")
+        if self.mode not in ("push", "pull"):
+            raise HxError(f"unknown all-reduce mode {self.mode!r}")
+        self.rank, self.tp, self.max_tok, self.hidden, self.sites = rank, tp, max_tok, hidden, sites
+        self._own, self._opened = [], []
+
+    def _alloc_own(self) -> dict:
+        lib = load()
+        slot_bytes = self.max_tok * self.hidden * 4
+        bufs = [("slot0", slot_bytes), ("slot1", slot_bytes)]
+        if self.mode == "pull":
+            bufs.append(("flags", self.sites * self.max_tok * 8 * 4))
+        else:
+            bufs.append(("inbox", int(lib.hx_tp_inbox_bytes(self.tp, self.max_tok, self.hidden))))
+        ptrs = {}
+        for name, nbytes in bufs:
+            ptrs[name] = _alloc(nbytes)
+            self._own.append(ptrs[name])
+        if self.mode == "push":
+            _check(lib.hx_tp_inbox_init(ptrs["inbox"], self.tp, self.max_tok, self.hidden, None), "hx_tp_inbox_init")
+            torch.cuda.synchronize()
+        return ptrs
+
+    def _finish(self, peer: dict):
+        self.peer = peer
+        self.site_state = torch.zeros(2 * self.sites, dtype=torch.int32, device="cuda")
+        self._arr = {name: (ctypes.c_void_p * self.tp)(*peer[name]) for name in peer}
 
     def slot(self, site: int) -> torch.Tensor:
         """This rank's partial slot for a call site, as a [max_tok, hidden] fp32 view."""
@@ -420,27 +454,37 @@ class PeerAllReduce:
             _p(self.site_state), _p(gain), _p(out), dtype_code(out.dtype) if out is not None else HX_F32,
             n_tok, self.hidden, eps, _stream()), "hx_tp_allreduce_residual_rmsnorm")
 
+    def close(self):
+        """Unmap the peers' buffers and free this rank's own (after a group
+        barrier, so no peer still maps them). Idempotent."""
+        if not getattr(self, "_own", None) and not getattr(self, "_opened", None):
+            return
+        lib = load()
+        torch.cuda.synchronize()
+        for q in self._opened:
+            lib.hx_ipc_close(q)
+        self._opened = []
+        if self._dist is not None:
+            self._dist.barrier(group=self._group)
+        for p in self._own:
+            lib.hx_ipc_free(p)
+        self._own = []
+
 
 # ---------------------------------------------------------------- NVLink P2P stage hand-off
 class P2PLink:
     """One directed decode hand-off link (sender device -> receiver device) of
     the inter-stage reshard (hx_handoff_push / hx_handoff_pull): the receiver
     owns a sentinel-armed inbox in cudaIpc memory, the sender maps it. Built
-    collectively by the two ranks over their 2-rank ``group``."""
+    collectively by the two ranks over their 2-rank ``group``.
+    ``P2PLink.local`` builds both ends in one process (single-GPU emulation)."""
 
     def __init__(self, src: int, dst: int, me: int, max_words: int, group, dist):
         lib = load()
-        self.src, self.dst, self.me = src, dst, me
-        self.max_words = (max_words + 3) // 4 * 4
-        self.state = torch.zeros(2, dtype=torch.int32, device="cuda")
+        self._init_state(src, dst, me, max_words)
         handle = None
-        self._own = self._peer = None
         if me == dst:
-            p = ctypes.c_void_p()
-            _check(lib.hx_ipc_alloc(ctypes.byref(p), int(lib.hx_handoff_inbox_bytes(self.max_words))), "hx_ipc_alloc")
-            self._own = p.value
-            _check(lib.hx_handoff_inbox_init(self._own, self.max_words, None), "hx_handoff_inbox_init")
-            torch.cuda.synchronize()
+            self._alloc_inbox()
             h = ctypes.create_string_buffer(64)
             _check(lib.hx_ipc_handle(self._own, h), "hx_ipc_handle")
             handle = h.raw
@@ -450,7 +494,33 @@ class P2PLink:
             q = ctypes.c_void_p()
             _check(lib.hx_ipc_open(next(h for h in got if h is not None), ctypes.byref(q)), "hx_ipc_open")
             self._peer = q.value
+            self._opened = True
+        self._group, self._dist = group, dist
         dist.barrier(group=group)
+
+    @classmethod
+    def local(cls, src: int, dst: int, max_words: int):
+        o = cls.__new__(cls)
+        o._init_state(src, dst, None, max_words)
+        o._alloc_inbox()
+        o._peer = o._own
+        o.recv_state = torch.zeros(2, dtype=torch.int32, device="cuda")   # each end keeps its own counter
+        o._group = o._dist = None
+        return o
+
+    def _init_state(self, src, dst, me, max_words):
+        self.src, self.dst, self.me = src, dst, me
+        self.max_words = (max_words + 3) // 4 * 4
+        self.state = torch.zeros(2, dtype=torch.int32, device="cuda")
+        self.recv_state = self.state
+        self._own = self._peer = None
+        self._opened = False
+
+    def _alloc_inbox(self):
+        lib = load()
+        self._own = _alloc(int(lib.hx_handoff_inbox_bytes(self.max_words)))
+        _check(lib.hx_handoff_inbox_init(self._own, self.max_words, None), "hx_handoff_inbox_init")
+        torch.cuda.synchronize()
 
     def push(self, t: torch.Tensor):
         """Sender: store ``t`` (contiguous, 32-bit words) into the receiver's inbox."""
@@ -461,7 +531,19 @@ class P2PLink:
     def pull(self, t: torch.Tensor):
         """Receiver: wait for this hand-off's data and copy it into ``t``."""
         _check(load().hx_handoff_pull(_p(t), self._own, t.numel() * t.element_size() // 4, self.max_words,
-                                      _p(self.state), _stream()), "hx_handoff_pull")
+                                      _p(self.recv_state), _stream()), "hx_handoff_pull")
+
+    def close(self):
+        lib = load()
+        torch.cuda.synchronize()
+        if self._opened:
+            lib.hx_ipc_close(self._peer)
+            self._opened = False
+        if self._dist is not None:
+            self._dist.barrier(group=self._group)
+        if self._own is not None:
+            lib.hx_ipc_free(self._own)
+            self._own = None
 
 
 def _tensor_at(ptr: int, shape) -> torch.Tensor:

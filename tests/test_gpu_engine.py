@@ -1,10 +1,11 @@
 """End-to-end parity of the engine on the B200 against the CPU oracle.
 
 fp32 mode: greedy ids identical, logits within 1e-3 relative (north star).
-bf16 mode (stated tolerance): teacher-forced logits within 2e-2 of the max
-|logit| at every step against the oracle run on the same bf16-rounded
-weights; free-running ids identical up to the first step whose oracle top-2
-margin is below the observed logit error."""
+bf16 mode (stated tolerance, oracle/parity.py = SURVEY §8(c)): teacher-forced
+logits within 2e-2 of max|logit| of the bf16-emulating oracle (3e-2 of the
+fp32-activation oracle) on the same bf16-rounded weights; top-1 agreement
+>= 99 % where the fp32 oracle's top-2 margin > 1e-2; the free-running first
+divergence is reported per sequence and must fall on an oracle near-tie."""
 
 from pathlib import Path
 
@@ -13,6 +14,7 @@ import pytest
 import torch
 
 from oracle.llama_oracle import Oracle, bf16_weights
+from oracle.parity import bf16_verdict
 from paper_2311_11514_b200 import ops
 from paper_2311_11514_b200.config import LlamaConfig, TINY, preset
 from paper_2311_11514_b200.engine import Engine, fused_epilogues
@@ -30,16 +32,23 @@ def tiny_oracle():
     return Oracle(TINY, init_host_weights(TINY, 0)).generate(G["prompt"], 16)
 
 
+@pytest.mark.parametrize("local_peer", [False, True], ids=["torch-sum", "peer-kernels"])
 @pytest.mark.parametrize("tps,layers", PLANS)
-def test_tiny_fp32_matches_golden_and_oracle(tps, layers, tiny_oracle):
+def test_tiny_fp32_matches_golden_and_oracle(tps, layers, local_peer, tiny_oracle):
+    """``local_peer``: the emulated ranks run on their own streams and the decode
+    step's all-reduces / hand-offs / token return go through the multi-GPU
+    kernels (hx_tp_allreduce_push_residual_rmsnorm, hx_handoff_push/pull)."""
     eng = Engine(simple_plan(tps, layers), TINY, dtype="fp32", batch=2, max_prompt=64, max_out=16,
-                 device="cuda:0", page_size=16)
+                 device="cuda:0", page_size=16, local_peer=local_peer)
     r = eng.generate(G["prompt"], 16, return_logits=True)
     ids, lg = tiny_oracle
     assert np.array_equal(r.ids, G["ids"])
     assert np.array_equal(r.ids, ids)
     assert np.abs(r.logits - lg).max() / np.abs(lg).max() < 1e-3
     assert np.abs(r.logits[..., G["cols"]] - G["col_val"]).max() / G["max_abs"] < 1e-3
+    if local_peer:   # the same through one CUDA graph per step over all rank streams, twice
+        for _ in range(2):
+            assert np.array_equal(eng.generate(G["prompt"], 16).ids, ids)
 
 
 def test_tiny_fp32_graph_replay_same_ids():
@@ -51,34 +60,22 @@ def test_tiny_fp32_graph_replay_same_ids():
     assert len(a.step_ms) == 15
 
 
-BF16_TOL_EMULATED = 2e-2   # vs the oracle that rounds activations where the engine does (random-init
-#                            nets amplify single bf16 rounding flips ~2-3x per block: measured 9.5e-3 on 7B widths)
-BF16_TOL_FP32ACT = 3e-2    # vs the fp32-activation oracle on the same bf16 weights
-
-
-def _bf16_check(cfg, tps, layers, b, s, s_out, page=64):
+def _bf16_check(cfg, tps, layers, b, s, s_out, page=64, local_peer=False):
+    """SURVEY §8(c) bf16 criteria (oracle/parity.py): teacher-forced logits vs
+    the bf16-emulating and the fp32-activation oracles, top-1 agreement on
+    positions with fp32 margin > 1e-2, and the first free-running divergence."""
     w = bf16_weights(init_host_weights(cfg, 0))
     prompt = synthetic_prompts(cfg, b, s, seed=1)
     ids_o, lg_o = Oracle(cfg, w, act_bf16=True, fused=fused_epilogues()).generate(prompt, s_out)
     eng = Engine(simple_plan(tps, layers), cfg, dtype="bf16", batch=b, max_prompt=s, max_out=s_out,
-                 device="cuda:0", page_size=page)
+                 device="cuda:0", page_size=page, local_peer=local_peer)
     r = eng.generate(prompt, s_out, forced=ids_o)
-    scale = np.abs(lg_o).max(axis=-1, keepdims=True)
-    err = np.abs(r.logits - lg_o) / scale
     _, lg_f = Oracle(cfg, w).generate(prompt, s_out, forced=ids_o)
-    err_f = np.abs(r.logits - lg_f) / np.abs(lg_f).max(axis=-1, keepdims=True)
-    print(f"bf16 teacher-forced max rel logit err: {err.max():.2e} (emulated), {err_f.max():.2e} (fp32 act)")
-    assert err.max() < BF16_TOL_EMULATED, err.max()
-    assert err_f.max() < BF16_TOL_FP32ACT, err_f.max()
-    srt = np.sort(lg_o, -1)
-    margin = (srt[..., -1] - srt[..., -2]) / scale[..., 0]
-    ok = margin > 2 * err.max()
-    agree = (r.ids.T == ids_o.T)[ok]
-    assert agree.mean() >= 0.99
-    # free-running: identical to the teacher-forced run up to its first divergence
     free = eng.generate(prompt, s_out)
-    assert np.array_equal(free.ids[:, 0], r.ids[:, 0])
-    return err.max()
+    v = bf16_verdict(r.logits, r.ids, lg_o, lg_f, free.ids, ids_o)
+    print(v.line())
+    assert v.ok, v.why
+    return v
 
 
 def test_tiny_bf16_tolerance():
@@ -104,13 +101,73 @@ def test_llama7b_shape_bf16_tcgen05_prefill_attention(monkeypatch):
     _bf16_check(cfg, [1], [2], 4, 128, 6)
 
 
+@pytest.mark.parametrize("local_peer", [False, True], ids=["torch-sum", "peer-kernels"])
 @pytest.mark.parametrize("fuse", FUSIONS)
-def test_gqa_asymmetric_bf16(fuse, monkeypatch):
+def test_gqa_asymmetric_bf16(fuse, local_peer, monkeypatch):
     """GQA group 8 per rank (70B-style head ratio) under an asymmetric [2,1] plan."""
     monkeypatch.setenv("HX_FUSE_SWIGLU", fuse[0])
     monkeypatch.setenv("HX_FUSE_ROPE", fuse[1])
     cfg = LlamaConfig("gqa-mini", 2, 2048, 16, 2, 5632, 32000)
-    _bf16_check(cfg, [2, 1], [1, 1], 4, 80, 6, page=32)
+    _bf16_check(cfg, [2, 1], [1, 1], 4, 80, 6, page=32, local_peer=local_peer)
+
+
+def test_llama70b_widths_emulated_42_peer_kernels():
+    """Llama-2-70B widths (H 8192, I 28672, 64:8 heads, V 32000), 2 layers under
+    the emulated asymmetric plan [4,2]: TP=4 shards (16 q / 2 kv heads per rank,
+    gate/up 14336 rows) then TP=2, the decode all-reduces in the NVLink push
+    kernel at both TP degrees and the 4 -> 2 hand-off + 2 -> 4 token return over
+    the P2P kernels, all on one GPU (per-rank streams)."""
+    cfg = preset("llama2-70b", num_layers=2)
+    _bf16_check(cfg, [4, 2], [1, 1], 4, 64, 6, local_peer=True)
+
+
+def test_llama7b_full_depth_c2():
+    """C2 exactly: Llama-2-7B, all 32 layers, b=8, s_in=512, host-seeded
+    weights, 4 teacher-forced steps (forced ids: seeded random tokens) against
+    the layer-streamed oracle (one causal pass over prompt + forced tokens).
+
+    * fp32 engine (fp32 weights + activations, SIMT kernels): the north-star
+      fp32 criterion -- argmax ids identical, logits within 1e-3 relative.
+    * bf16 engine (the bench's configuration): SURVEY §8(c) criteria, with the
+      tolerance scaled to depth: the engine may deviate from the bf16-emulating
+      oracle by at most max(2e-2, 1.5 x the deviation between the two oracles
+      that differ only in rounding activations to bf16) -- the spread that
+      bf16 activation storage alone causes at this depth -- and top-1 must
+      agree >= 99 % where the fp32 oracle's margin exceeds twice that bound."""
+    from oracle.llama_oracle import streamed_teacher_forced
+    from oracle.parity import rel_err, top2_margin
+    assert fused_epilogues() == (False, False)
+    cfg = preset("llama2-7b")
+    b, s, k = 8, 512, 4
+    prompt = synthetic_prompts(cfg, b, s, seed=1)
+    forced = np.random.default_rng(2).integers(0, cfg.vocab, (b, k)).astype(np.int32)
+    runs = {}
+    for dt in ("fp32", "bf16"):
+        eng = Engine(simple_plan([1], [32]), cfg, dtype=dt, batch=b, max_prompt=s, max_out=k, device="cuda:0")
+        runs[dt] = eng.generate(prompt, k, forced=forced)
+        del eng
+        torch.cuda.empty_cache()
+    seq = np.concatenate([prompt, forced[:, :k - 1]], 1)
+    lg = streamed_teacher_forced(cfg, 0, seq, range(s - 1, s + k - 1),
+                                 modes=((False, False), (True, True), (True, False)))
+    f32, emu, bact32 = lg[(False, False)], lg[(True, True)], lg[(True, False)]
+    r32 = runs["fp32"]
+    err32 = rel_err(r32.logits, f32).max()
+    print(f"C2 fp32: max rel logit err {err32:.2e}, ids equal {np.array_equal(r32.ids.T, f32.argmax(-1))}")
+    assert np.array_equal(r32.ids.T, f32.argmax(-1))
+    assert err32 < 1e-3
+    rb = runs["bf16"]
+    floor = rel_err(emu, bact32).max()          # oracle vs oracle: bf16 activation storage alone
+    tol = max(2e-2, 1.5 * floor)
+    err = rel_err(rb.logits, emu).max()
+    err_f = rel_err(rb.logits, bact32).max()
+    ok = top2_margin(f32) > 2 * tol
+    agree = (rb.ids.T == emu.argmax(-1))[ok]
+    print(f"C2 bf16: err {err:.2e} vs emulated oracle, {err_f:.2e} vs fp32-act oracle; oracle-vs-oracle "
+          f"floor {floor:.2e} -> tol {tol:.2e}; top-1 agreement {agree.mean() if agree.size else 1:.3f} on "
+          f"{agree.size} positions with margin > {2 * tol:.2e}")
+    assert err < tol and err_f < tol + floor
+    assert agree.size == 0 or agree.mean() >= 0.99
 
 
 def test_kernel_launches_are_counted():
