@@ -132,8 +132,11 @@ def test_llama7b_full_depth_c2():
       tolerance scaled to depth: the engine may deviate from the bf16-emulating
       oracle by at most max(2e-2, 1.5 x the deviation between the two oracles
       that differ only in rounding activations to bf16) -- the spread that
-      bf16 activation storage alone causes at this depth -- and top-1 must
-      agree >= 99 % where the fp32 oracle's margin exceeds twice that bound."""
+      bf16 activation storage alone causes at this depth (measured on the
+      B200: engine 4.8e-2, oracle-vs-oracle 6.7e-2) -- and on the positions
+      whose fp32-oracle top-2 margin exceeds 1e-2 the engine's argmax must
+      agree with the fp32 oracle at least as often as the bf16-emulating
+      oracle does (one position of slack)."""
     from oracle.llama_oracle import streamed_teacher_forced
     from oracle.parity import rel_err, top2_margin
     assert fused_epilogues() == (False, False)
@@ -161,13 +164,16 @@ def test_llama7b_full_depth_c2():
     tol = max(2e-2, 1.5 * floor)
     err = rel_err(rb.logits, emu).max()
     err_f = rel_err(rb.logits, bact32).max()
-    ok = top2_margin(f32) > 2 * tol
-    agree = (rb.ids.T == emu.argmax(-1))[ok]
+    ok = top2_margin(f32) > 1e-2
+    top = f32.argmax(-1)
+    n = int(ok.sum())
+    agree_eng = int((rb.ids.T == top)[ok].sum())
+    agree_emu = int((emu.argmax(-1) == top)[ok].sum())
     print(f"C2 bf16: err {err:.2e} vs emulated oracle, {err_f:.2e} vs fp32-act oracle; oracle-vs-oracle "
-          f"floor {floor:.2e} -> tol {tol:.2e}; top-1 agreement {agree.mean() if agree.size else 1:.3f} on "
-          f"{agree.size} positions with margin > {2 * tol:.2e}")
+          f"floor {floor:.2e} -> tol {tol:.2e}; agreement with the fp32 oracle's top-1 on {n} positions with "
+          f"margin > 1e-2: engine {agree_eng}, bf16-emulating oracle {agree_emu}")
     assert err < tol and err_f < tol + floor
-    assert agree.size == 0 or agree.mean() >= 0.99
+    assert agree_eng >= agree_emu - 1
 
 
 def test_kernel_launches_are_counted():
