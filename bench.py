@@ -7,24 +7,28 @@ A step is one request batch through ``Engine.generate`` (prefill, then
 s_out - 1 greedy decode steps, CUDA graphs per stage). Workloads (BASELINE.json
 configs; synthetic prompts, random-init weights of the named architecture):
 
-  N=1  Llama-2-7B bf16, plan [1] (32 layers), b=8, 512/128      (configs[1])
-  N=2  Llama-2-70B bf16, plan [1,1] layers 42/38, b=32, 1024/256
-  N=4  Llama-2-70B bf16, plan [2,1,1] layers 40/20/20, b=32, 1024/256
-  N=8  Llama-2-70B bf16, plan [4,2,2] layers 40/20/20, b=32, 1024/256 (configs[3])
+  N=1  c2       Llama-2-7B bf16, plan [1] (32 layers), b=8, 512/128      (configs[1])
+  N=2  70b-pp2  Llama-2-70B bf16, plan [1,1] layers 42/38, b=32, 1024/256
+  N=3  c3-asym  Llama-2-13B bf16, plan [2,1] layers 28/12, b=8, 512/128 (configs[2])
+  N=4  70b-pp3  Llama-2-70B bf16, plan [2,1,1] layers 40/20/20, b=32, 1024/256
+       c3-sym   Llama-2-13B bf16, plan [2,2] layers 20/20, b=8, 512/128 (--workload c3-sym; configs[2])
+  N=8  c4       Llama-2-70B bf16, plan [4,2,2] layers 40/20/20, b=32, 1024/256 (configs[3])
 
 ``value`` = decode tokens/s = b * (s_out - 1) * K / (sum of decode-phase device
 time, CUDA events, on the last stage -- first to last generated token -- max
 over its ranks), inputs resident. ``e2e`` = generated
 tokens/s through the public API with host prompts in and host ids out
-(b * s_out per request / wall time of generate, prefill included).
+(b * s_out per request / wall time of generate, prefill included) -- the
+same unit and definition in both arms.
 Weights (13.5-140 GB) are far larger than the 126 MB L2, so every decode step
 streams them from HBM; no L2 flush is needed.
 
 ``--impl reference`` times the CPU oracle port (oracle/llama_oracle.py, the
 only CPU implementation of the path; the reference repo has none) on the
-host cores for the same workload: one transformer layer decode step at the
-config shape (batch b, mid-generation context) + lm_head, extrapolated to all
-layers, per step.
+host cores for the same workload: per step, one transformer layer decode step
+at the config shape (batch b, mid-generation context) + lm_head, and one layer
+prefill of one prompt + lm_head row, extrapolated to all layers and prompts
+(value = decode tok/s, e2e = b * s_out / (prefill + (s_out - 1) decode steps)).
 """
 
 from __future__ import annotations
@@ -48,11 +52,14 @@ METRIC = "decode tokens/s (greedy, b x (s_out-1) / decode time)"
 UNIT = "tok/s"
 
 WORKLOADS = {
-    1: dict(model="llama2-7b", tps=[1], layers=[32], batch=8, s_in=512, s_out=128),
-    2: dict(model="llama2-70b", tps=[1, 1], layers=[42, 38], batch=32, s_in=1024, s_out=256),
-    4: dict(model="llama2-70b", tps=[2, 1, 1], layers=[40, 20, 20], batch=32, s_in=1024, s_out=256),
-    8: dict(model="llama2-70b", tps=[4, 2, 2], layers=[40, 20, 20], batch=32, s_in=1024, s_out=256),
+    "c2": dict(model="llama2-7b", tps=[1], layers=[32], batch=8, s_in=512, s_out=128),
+    "70b-pp2": dict(model="llama2-70b", tps=[1, 1], layers=[42, 38], batch=32, s_in=1024, s_out=256),
+    "70b-pp3": dict(model="llama2-70b", tps=[2, 1, 1], layers=[40, 20, 20], batch=32, s_in=1024, s_out=256),
+    "c4": dict(model="llama2-70b", tps=[4, 2, 2], layers=[40, 20, 20], batch=32, s_in=1024, s_out=256),
+    "c3-asym": dict(model="llama2-13b", tps=[2, 1], layers=[28, 12], batch=8, s_in=512, s_out=128),
+    "c3-sym": dict(model="llama2-13b", tps=[2, 2], layers=[20, 20], batch=8, s_in=512, s_out=128),
 }
+BY_GPUS = {1: "c2", 2: "70b-pp2", 3: "c3-asym", 4: "70b-pp3", 8: "c4"}
 
 
 def peaks():
@@ -64,7 +71,7 @@ def peaks():
 
 
 def workload(n, args):
-    w = dict(WORKLOADS.get(n, WORKLOADS[1]))
+    w = dict(WORKLOADS[args.workload or BY_GPUS.get(n, "c2")])
     if args.model:
         w["model"] = args.model
     if args.plan:
@@ -80,6 +87,28 @@ def workload(n, args):
 def wl_name(w):
     return (f"{w['model']} bf16 plan [{','.join(map(str, w['tps']))}] layers "
             f"{'/'.join(map(str, w['layers']))} b={w['batch']} {w['s_in']}/{w['s_out']}")
+
+
+def config_dict(w, cfg):
+    """The workload, identical in both arms' JSON lines."""
+    return {"workload": wl_name(w), "model": cfg.name, "plan": w["tps"], "layers": w["layers"],
+            "global_batch": w["batch"], "seq_len": w["s_in"], "decode_tokens": w["s_out"],
+            "parallelism": "pp%d-tp[%s]" % (len(w["tps"]), ",".join(map(str, w["tps"]))),
+            "l2": "weights stream from HBM each step (>> 126 MB L2); no flush"}
+
+
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+E2E_UNIT = "tok/s"
+E2E_DEF = "b x s_out generated tokens per request / request wall time, host prompt in -> host ids out (prefill included)"
 
 
 # ----------------------------------------------------------------- accounting
@@ -157,20 +186,24 @@ class ClockSampler:
 _CPU_WEIGHTS: dict = {}
 
 
+def _cpu_weights(cfg, seed):
+    """Layer 0 + final norm + lm_head (weight generation is setup, not timed)."""
+    from paper_2311_11514_b200.weights import init_globals, layer_stream
+    key = (cfg, seed)
+    if key not in _CPU_WEIGHTS:
+        _, lw = next(layer_stream(cfg, seed, [0], lookahead=0))
+        _CPU_WEIGHTS[key] = {"layers": {0: lw}, **init_globals(cfg, seed, ("norm", "lm_head"))}
+    return _CPU_WEIGHTS[key]
+
+
 def cpu_decode_sample(cfg, w, steps=2, seed=0):
     """Time the CPU oracle on one layer's decode step at the config shape
     (batch b, context = mean generation context) + final norm + lm_head;
     return extrapolated decode tok/s for the full model (all host threads)."""
     from oracle.llama_oracle import Cache, Oracle
-    from paper_2311_11514_b200.weights import LAYER_TENSORS, init_tensor
     b = w["batch"]
     ctx = int(w["s_in"] + (w["s_out"] - 1) / 2)
-    key = (cfg, seed)
-    if key not in _CPU_WEIGHTS:  # weight generation is setup, not part of the timed sample
-        lw = {n: init_tensor(cfg, seed, n, 0) for n in LAYER_TENSORS}
-        head = {"norm": init_tensor(cfg, seed, "norm"), "lm_head": init_tensor(cfg, seed, "lm_head")}
-        _CPU_WEIGHTS[key] = {"layers": {0: lw}, **head}
-    orc = Oracle(cfg, _CPU_WEIGHTS[key])
+    orc = Oracle(cfg, _cpu_weights(cfg, seed))
     rng = np.random.default_rng(0)
     times = []
     for _ in range(steps):
@@ -188,6 +221,21 @@ def cpu_decode_sample(cfg, w, steps=2, seed=0):
     return b / step_s, step_s
 
 
+def cpu_prefill_sample(cfg, w, seed=0):
+    """Time the CPU oracle on one layer's prefill of ONE prompt (s_in tokens)
+    + the lm_head row; return the extrapolated prefill seconds of the whole
+    request: x b sequences (independent, same cost) x L layers."""
+    from oracle.llama_oracle import Cache, Oracle
+    orc = Oracle(cfg, _cpu_weights(cfg, seed))
+    x = np.random.default_rng(0).standard_normal((1, w["s_in"], cfg.hidden_dim), dtype=np.float32)
+    t0 = time.perf_counter()
+    y = orc.layer(0, x, 0, Cache())
+    t1 = time.perf_counter()
+    orc.logits(y[:, -1])
+    t2 = time.perf_counter()
+    return w["batch"] * (t1 - t0) * cfg.num_layers + w["batch"] * (t2 - t1)
+
+
 def run_reference(args, w, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -197,20 +245,29 @@ def run_reference(args, w, cfg):
     torch.set_num_threads(cores)
     for _ in range(max(0, args.warmup)):
         cpu_decode_sample(cfg, w, steps=1)
-    vals, t0 = [], time.perf_counter()
+        cpu_prefill_sample(cfg, w)
+    vals, e2es, t0 = [], [], time.perf_counter()
+    b, s_out = w["batch"], w["s_out"]
     for _ in range(args.steps):
-        v, _ = cpu_decode_sample(cfg, w, steps=1)
+        v, step_s = cpu_decode_sample(cfg, w, steps=1)
+        pre_s = cpu_prefill_sample(cfg, w)
         vals.append(v)
+        e2es.append(b * s_out / (pre_s + (s_out - 1) * step_s))
     wall = time.perf_counter() - t0
     value = float(np.mean(vals))
-    sample = (f"CPU oracle port (numpy fp32, {cores} threads): one {cfg.name} layer decode step at "
-              f"b={w['batch']}, ctx={int(w['s_in'] + (w['s_out'] - 1) / 2)} + lm_head, x{cfg.num_layers} layers")
+    e2e = float(np.mean(e2es))
+    sample = (f"CPU oracle port (numpy fp32, {cores} threads, {cpu_model()}): per step one {cfg.name} layer "
+              f"decode step at b={b}, ctx={int(w['s_in'] + (s_out - 1) / 2)} + lm_head (x{cfg.num_layers} layers) "
+              f"and one layer prefill of one {w['s_in']}-token prompt + lm_head row (x{b} prompts x"
+              f"{cfg.num_layers} layers); e2e = b*s_out / (prefill + (s_out-1) decode steps), extrapolated")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / max(1, args.steps) * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic", "config": {"workload": wl_name(w) + " (CPU oracle, extrapolated)"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "data": "synthetic", "config": config_dict(w, cfg),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+                             "cpu_model": cpu_model()},
+            "e2e": {"value": e2e, "unit": E2E_UNIT, "definition": E2E_DEF, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
 
@@ -279,16 +336,16 @@ def gemm_roofline(eng, cfg, w, hbm, reps=5):
         per_shape[name] = {"shape": list(sub[0][0].shape), "us_per_launch": round(ts / len(sub) * 1e6, 2),
                            "GBps": round(gb / ts / 1e9, 1)}
     traffic = None
-    tfile = ROOT / "profiles" / "r01" / "gemm_traffic_7b.json"
+    tfile = ROOT / "profiles" / "r02" / "gemm_traffic.json"
     if cfg.name == "llama2-7b" and w["batch"] == 8 and tfile.exists():
-        # dram read+write per launch from one ncu --set full capture of the same
-        # kernel on this workload (one layer's qkv/o/gate_up/down), for comparison
-        # with the algorithmic bytes per launch
+        # dram read+write per launch from ncu --set full captures of the same
+        # kernel at this workload's four layer shapes (one launch per shape, each
+        # in its own process: tools/gemm_traffic.py), against the algorithmic
+        # bytes per launch
         tj = json.loads(tfile.read_text())
-        traffic = {"bytes_per_launch": round(tj["traffic_bytes_per_launch_avg"]),
-                   "algorithmic_bytes_per_launch": round(tj["algorithmic_bytes_per_launch_avg"]),
-                   "ratio": round(tj["traffic_bytes_per_launch_avg"] / tj["algorithmic_bytes_per_launch_avg"], 4),
-                   "source": "profiles/r01/gemm_traffic_7b.json"}
+        tr, al = tj["traffic_bytes_per_launch_avg_7b_layer"], tj["algorithmic_bytes_per_launch_avg_7b_layer"]
+        traffic = {"bytes_per_launch": round(tr), "algorithmic_bytes_per_launch": round(al),
+                   "ratio": round(tr / al, 4), "source": "profiles/r02/gemm_traffic.json"}
     return {"bound": "hbm", "kernel": "hx_linear (tcgen05 stream-K decode GEMM)", "achieved": round(achieved, 1),
             "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": traffic,
             "launches_per_step": len(seq), "avg_launch_us": round(t / len(seq) * 1e6, 2),
@@ -301,6 +358,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="hexgen", choices=["hexgen", "reference"])
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), help="default by --gpus: " + str(BY_GPUS))
     ap.add_argument("--model")
     ap.add_argument("--plan")
     ap.add_argument("--layers")
@@ -386,7 +444,7 @@ def main():
         import torch as _t
         _t.set_num_threads(os.cpu_count())
         v, st = cpu_decode_sample(cfg, w, steps=2)
-        cpu = {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+        cpu = {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "cpu_model": cpu_model(),
                "sample": f"CPU oracle (numpy fp32): 1 {cfg.name} layer decode step b={b} ctx={int(s_in + (s_out - 1) / 2)}"
                          f" + lm_head, x{cfg.num_layers} layers ({st * 1e3:.0f} ms/step extrapolated)"}
     if rank == 0:
@@ -394,10 +452,7 @@ def main():
             "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(wall / args.steps * 1e3, 3), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, uniform prompts seed 1)",
-            "config": {"workload": wl_name(w), "model": cfg.name, "plan": w["tps"], "layers": w["layers"],
-                       "global_batch": b, "seq_len": s_in, "decode_tokens": s_out,
-                       "parallelism": "pp%d-tp[%s]" % (len(w["tps"]), ",".join(map(str, w["tps"]))),
-                       "l2": "weights stream from HBM each step (>> 126 MB L2); no flush"},
+            "config": config_dict(w, cfg),
             "p50_decode_step_ms": round(p50, 4) if p50 else None,
             "p90_decode_step_ms": round(float(np.percentile(steps_ms, 90)), 4) if steps_ms else None,
             "prefill_ms": round(pre_s / args.steps * 1e3, 3),
@@ -408,7 +463,7 @@ def main():
                               "frac": round(step_rf * 1e3 / p50, 4) if p50 else None,
                               "peak_gbs": hbm, "peak_kind": peak_kind},
             "roofline": roof,
-            "e2e": {"value": round(e2e, 2), "unit": "tok/s (generated incl. prefill, host->host)",
+            "e2e": {"value": round(e2e, 2), "unit": E2E_UNIT, "definition": E2E_DEF,
                     "h2d_bytes_per_step": b * s_in * 4, "d2h_bytes_per_step": b * s_out * 4},
             "gpu_launches": launches,
             "clocks": clk,
