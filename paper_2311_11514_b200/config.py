@@ -31,6 +31,7 @@ class LlamaConfig:
     rms_eps: float = 1e-5
     rope_theta: float = 10000.0
     bytes_per_param: int = 2
+    head_dim_override: int = 0   # 0: hidden_dim // num_heads (a TP shard viewed as a model sets it)
 
     def __post_init__(self):
         if self.hidden_dim % self.num_heads:
@@ -40,7 +41,7 @@ class LlamaConfig:
 
     @property
     def head_dim(self) -> int:
-        return self.hidden_dim // self.num_heads
+        return self.head_dim_override or self.hidden_dim // self.num_heads
 
     @property
     def group(self) -> int:

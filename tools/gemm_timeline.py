@@ -22,6 +22,17 @@ model = next((a for a in sys.argv[1:] if not a.startswith("-")), "llama2-7b")
 full = "--full-step" in sys.argv
 cfg = preset(model)
 b, s_in = 8, 512
+# --tp N: one TP rank of a stage, as a single-GPU model whose layers have exactly
+# that rank's shard shapes (heads, kv heads, intermediate and vocab divided by N)
+tp = int(next((a.split("=")[1] for a in sys.argv if a.startswith("--tp=")), "1"))
+if tp > 1:
+    from dataclasses import replace
+    cfg = replace(cfg, head_dim_override=cfg.head_dim, num_heads=cfg.num_heads // tp, num_kv_heads=cfg.num_kv_heads // tp,
+                  intermediate=cfg.intermediate // tp, vocab=cfg.vocab // tp)
+if model == "llama2-70b":
+    b, s_in = 32, 1024
+    cfg = __import__("dataclasses").replace(cfg, num_layers=int(next(
+        (a.split("=")[1] for a in sys.argv if a.startswith("--layers=")), "20")))
 eng = Engine(simple_plan([1], [cfg.num_layers]), cfg, dtype="bf16", batch=b, max_prompt=s_in, max_out=4,
              device="cuda:0", weights="device", use_graphs=False)
 prompt = np.random.default_rng(1).integers(0, cfg.vocab, size=(b, s_in), dtype=np.int32)
