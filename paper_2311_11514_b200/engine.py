@@ -927,6 +927,22 @@ class Engine:
         hist = last[0].history[:b, :s_out] if last else None
         return self.comm.broadcast_ids(hist, b, s_out, self.roles[-1].tp_group[0], self.device)
 
+    def close(self):
+        """Release the NVLink peer state (unmap peers' IPC buffers, free own
+        ones, after a group barrier) and the captured graphs. Idempotent."""
+        self._graphs = None
+        links = {}
+        for e in self.execs:
+            if e.par is not None:
+                e.par.close()
+                e.par = None
+            for link in list(e.p2p_send) + list(e.ids_send) + [e.p2p_recv, e.ids_recv]:
+                if link is not None:
+                    links[id(link)] = link      # an emulated link is held by both of its ends
+            e.p2p_send, e.ids_send, e.p2p_recv, e.ids_recv = [], [], None, None
+        for link in links.values():
+            link.close()
+
     def service_time(self, task: TaskSpec, prompt=None) -> float:
         """Measured seconds for one request of this shape (the value the
         reference's ``service_times`` table holds, simulate.py:135-142)."""

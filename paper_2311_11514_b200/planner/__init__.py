@@ -34,6 +34,6 @@ from .pool import (B200, Bucket, ClusterSpec, Device, GpuType, TypeVector, a100_
                    build_cluster, cluster_from_dict, cluster_to_dict, llama70b, load_cluster, remove_devices,
                    three_tier_cluster, toy_model, two_region_cluster)
 from .slo_sim import (MeasuredServiceModel, SloConfig, SloReport, WorkloadSpec, generate_workload, load_slo,
-                      load_workload, pipeline_shape, service_times, simulate, sweep_rate, sweep_slo_scale)
+                      load_workload, pipeline_shape, place_shape, service_times, simulate, sweep_rate, sweep_slo_scale)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -18,21 +18,31 @@ import numpy as np
 
 from .config import LlamaConfig
 from .engine import Engine
-from .plan import GlobalAssignment, TaskSpec
+from .plan import GlobalAssignment, InputError, TaskSpec
 
 
 def measured_service_times(assignment: GlobalAssignment, cfg: LlamaConfig, tasks: Iterable[TaskSpec],
                            cluster=None, *, comm: str = "local", device=None, dtype: str = "bf16",
                            weights: str = "device", repeats: int = 1, seed: int = 1,
-                           kernels=None) -> dict:
+                           kernels=None, emulated: bool = False) -> dict:
     """{(replica index, TaskSpec): seconds} for every pipeline and distinct shape.
 
-    ``comm='local'`` emulates each pipeline's ranks in this process on
-    ``device``; ``comm='dist'`` runs under torchrun where this process's rank
-    is a device of the (single) pipeline. ``cluster`` is accepted for
+    ``comm='local'`` measures single-GPU replicas in this process on
+    ``device`` (multi-GPU replicas only with ``emulated=True``: their ranks
+    then run one after another, so the seconds are not a service time);
+    ``comm='dist'`` runs under torchrun where this process's rank is a device
+    of the (single) pipeline. Each engine is closed (peer mappings, IPC
+    buffers) before the next is built. ``cluster`` is accepted for
     signature parity with the reference and unused: the hardware is measured.
     """
     shapes = sorted(set(tasks), key=lambda t: (t.batch_size, t.input_len, t.output_len))
+    if comm == "local" and not emulated:
+        wide = [r for r, pipe in enumerate(assignment.pipelines) if sum(len(st.devices) for st in pipe) > 1]
+        if wide:
+            raise InputError(f"replicas {wide} span several GPUs: comm='local' would run their ranks one after "
+                             "another on one device, which is not their service time -- measure them under "
+                             "torchrun (comm='dist', tools/measure_service.py) or pass emulated=True for a "
+                             "functional (untimed-semantics) run")
     table = {}
     for r in range(len(assignment.pipelines)):
         for task in shapes:
@@ -44,5 +54,6 @@ def measured_service_times(assignment: GlobalAssignment, cfg: LlamaConfig, tasks
             eng.generate(prompt, task.output_len)  # warm-up + graph capture
             ts = [eng.service_time(task, prompt) for _ in range(max(1, repeats))]
             table[(r, task)] = float(np.median(ts))
+            eng.close()
             del eng
     return table

@@ -52,8 +52,11 @@ def test_measured_service_times_has_reference_table_shape():
     ga = GlobalAssignment(((StageAssignment((0, 1), 3), StageAssignment((2,), 1)),
                            (StageAssignment((3,), 4),)))
     tasks = [TaskSpec(2, 8, 3), TaskSpec(2, 8, 3), TaskSpec(2, 16, 2)]
+    with pytest.raises(InputError):   # a multi-GPU replica is not timed by emulation
+        measured_service_times(ga, TINY, tasks, comm="local", device="cpu", dtype="fp32",
+                               weights="host", kernels=cpu_kernels)
     tab = measured_service_times(ga, TINY, tasks, comm="local", device="cpu", dtype="fp32",
-                                 weights="host", kernels=cpu_kernels)
+                                 weights="host", kernels=cpu_kernels, emulated=True)
     assert set(tab) == {(r, t) for r in range(2) for t in set(tasks)}
     assert all(v > 0 for v in tab.values())
 

@@ -9,6 +9,8 @@ import subprocess
 import sys
 from pathlib import Path
 
+import pytest
+
 from paper_2311_11514_b200 import planner as P
 from paper_2311_11514_b200.planner import cmdline
 
@@ -80,7 +82,7 @@ def test_plan_with_measured_service_model(tmp_path):
     meas = tmp_path / "meas"
     meas.mkdir()
     for i, (tps, layers) in enumerate((((2, 2), (40, 40)), ((2,), (80,)), ((4,), (80,)))):
-        pipe = cmdline._place_shape(tuple(zip(tps, layers)), cluster)
+        pipe = P.place_shape(tuple(("b200", tp, l) for tp, l in zip(tps, layers)), cluster)
         secs = P.pipeline_cost(pipe, model, task, cluster)[0]
         (meas / f"p{i}.json").write_text(json.dumps({
             "plan": "[" + ",".join(map(str, tps)) + "]", "layers": list(layers), "seconds": secs,
@@ -100,3 +102,40 @@ def test_plan_with_measured_service_model(tmp_path):
     plan = P.load_plan(tmp_path / "b" / "plan.json")
     assert sorted(d for pipe in plan.pipelines for st in pipe for d in st.devices) == sorted(
         set(d for pipe in plan.pipelines for st in pipe for d in st.devices))
+    # the measurements are what the search optimised: measured shapes answer with
+    # their measured seconds, and the fitness differs from the closed-form run
+    svc = cmdline.load_service(svc_dir, model, cluster, per_replica_ok=False)
+    for (shape, t), secs in svc.measured.items():
+        assert svc(P.place_shape(shape, cluster), t) == secs
+    fit_meas = json.loads((tmp_path / "b" / "plan.json").read_text())["fitness"]
+    fit_closed = json.loads(gold.read_text())["fitness"]
+    assert fit_meas != fit_closed
+    # a replica-indexed table is accepted by simulate only
+    table = tmp_path / "table.json"
+    table.write_text(json.dumps({"entries": [{"replica": 0, "batch_size": task.batch_size, "input_len": task.input_len,
+                                              "output_len": task.output_len, "seconds": 1.0}]}))
+    with pytest.raises(P.InputError):
+        cmdline.load_service(table, model, cluster, per_replica_ok=False)
+    assert cmdline.load_service(table, model, cluster, per_replica_ok=True) == {(0, task): 1.0}
+
+
+def test_measured_service_model_keys_by_gpu_type():
+    """a measurement on one GPU type must not answer for the same
+    (TP, layers) shape on another type; unmeasured types use their own scale."""
+    cluster = P.three_tier_cluster()
+    model = P.toy_model()
+    task = P.TaskSpec(4, 64, 16)
+    types = sorted({d.gpu_type.type_id for d in cluster.devices})
+    t0 = types[0]
+    shape = ((t0, 1, model.num_layers),)
+    pipe0 = P.place_shape(shape, cluster)
+    closed0 = P.pipeline_cost(pipe0, model, task, cluster)[0]
+    svc = P.MeasuredServiceModel({(shape, task): 2.0 * closed0}, model, cluster)
+    assert svc(pipe0, task) == 2.0 * closed0
+    for t in types[1:]:
+        other = P.place_shape(((t, 1, model.num_layers),), cluster)
+        if other is None:
+            continue
+        closed = P.pipeline_cost(other, model, task, cluster)[0]
+        assert svc(other, task) == pytest.approx(2.0 * closed)   # calibrated closed form, not t0's seconds
+        assert svc(other, task) != 2.0 * closed0 or closed == closed0

@@ -8,7 +8,7 @@ The pipeline's stages keep their TP degrees and layer counts; its device ids
 are renumbered 0..n-1 in stage order (every B200 of an NVSwitch node is
 equivalent), so one pipeline of an 8-GPU plan is measured on n GPUs. Rank 0
 writes ``{"replica", "batch_size", "input_len", "output_len", "seconds",
-"prefill_s", "decode_s", "plan"}`` -- an entry of the ``--service`` table of
+"prefill_s", "decode_s", "plan", "layers", "gpu_type"}`` -- an entry of the ``--service`` table of
 ``python -m paper_2311_11514_b200.planner simulate``.
 """
 import argparse
@@ -35,6 +35,7 @@ def main():
     ap.add_argument("--model", default="llama2-70b")
     ap.add_argument("--task", default="32,1024,256")
     ap.add_argument("--repeats", type=int, default=2)
+    ap.add_argument("--gpu-type", default="b200", help="cluster GPU type id the measurement applies to")
     ap.add_argument("--out", required=True)
     a = ap.parse_args()
     pipe = load_plan(a.plan).pipelines[a.pipeline]
@@ -67,7 +68,8 @@ def main():
         doc = {"replica": a.pipeline, "batch_size": task.batch_size, "input_len": task.input_len,
                "output_len": task.output_len, "seconds": float(statistics.median(v[:, 0])),
                "prefill_s": float(statistics.median(v[:, 1])), "decode_s": float(statistics.median(v[:, 2])),
-               "plan": plan_notation(pipe), "layers": [s.num_layers for s in pipe], "gpus": d}
+               "plan": plan_notation(pipe), "layers": [s.num_layers for s in pipe], "gpus": d,
+               "gpu_type": a.gpu_type, "device_name": torch.cuda.get_device_name(dev)}
         Path(a.out).write_text(json.dumps(doc, indent=1) + "\n")
         print(json.dumps(doc), flush=True)
     if world > 1:
