@@ -12,11 +12,15 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from tools.gemm_traffic import SHAPES, algorithmic_bytes  # noqa: E402
 
 METRICS = ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum",
-           "dram__throughput.avg.pct_of_peak_sustained_elapsed", "launch__grid_size", "Kernel Name"]
+           "dram__bytes_read.sum.pct_of_peak_sustained_elapsed", "launch__grid_size", "Kernel Name"]
 
 
-def read(rep):
-    out = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+def read(path):
+    path = Path(path)
+    if path.suffix == ".csv":
+        out = path.read_text()
+    else:
+        out = subprocess.run(["ncu", "-i", str(path), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units, vals = rows[0], rows[1], rows[2]
     d = {}
@@ -42,7 +46,9 @@ def main(src, dst):
                      "python tools/gemm_traffic.py run <shape> (one launch after a 256 MB L2 flush)",
            "shapes": {}}
     for name, (n_tok, n_out, k) in SHAPES.items():
-        rep = Path(src) / f"{name}.ncu-rep"
+        rep = Path(src) / f"{name}.csv"
+        if not rep.exists():
+            rep = Path(src) / f"{name}.ncu-rep"
         if not rep.exists():
             continue
         d = read(rep)
@@ -54,7 +60,7 @@ def main(src, dst):
                                "dram_read": rd, "dram_write": wr, "algorithmic_bytes": alg,
                                "traffic_over_algorithmic": round((rd + wr) / alg, 4), "ncu_us": us,
                                "ncu_GBps_algorithmic": round(alg / us / 1e3, 1),
-                               "dram_pct_peak": float(d["dram__throughput.avg.pct_of_peak_sustained_elapsed"][0])}
+                               "dram_pct_peak": float(d["dram__bytes_read.sum.pct_of_peak_sustained_elapsed"][0])}
     s7 = [v for n, v in res["shapes"].items() if n.startswith("7b_") and "lm_head" not in n]
     if s7:
         res["traffic_bytes_per_launch_avg_7b_layer"] = sum(v["dram_read"] + v["dram_write"] for v in s7) / len(s7)
