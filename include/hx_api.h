@@ -249,6 +249,17 @@ int hx_attn_decode_rope_append(const void *qkv, void *k_cache, void *v_cache,
                                int page_size, int max_blocks, int max_ctx, float theta,
                                void *workspace, size_t workspace_bytes,
                                hx_stream_t stream);
+/* hx_attn_decode_rope_append for a QKV projection run as a deferred decode GEMM
+ * (hx_linear(..., HX_LINEAR_DEFER_REDUCE) into fp32 qkv32 [batch][ld_qkv], its
+ * workspace gemm_workspace, inner dimension k_dim): the kernel sums the split
+ * tiles' partials in CTA order and rounds to bf16 (the bits the GEMM's fix-up
+ * would have stored), so the GEMM has no fix-up tail. Same outputs as
+ * hx_linear (bf16 qkv) + hx_attn_decode_rope_append, bit for bit. */
+int hx_attn_decode_rope_append_sk(const float *qkv32, int ld_qkv, const void *gemm_workspace, int k_dim,
+                                  void *k_cache, void *v_cache, const int32_t *block_table,
+                                  const int32_t *seq_lens, void *o, int batch, int hq, int hkv, int hd,
+                                  int page_size, int max_blocks, int max_ctx, float theta, void *workspace,
+                                  size_t workspace_bytes, hx_stream_t stream);
 
 /* Causal prefill attention: q [batch*s, hq, hd] (roped), keys/values are the
  * s prompt tokens already appended to the paged cache (positions

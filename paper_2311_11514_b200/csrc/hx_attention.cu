@@ -19,7 +19,7 @@ int launch_decode_mma(int G, int hd, dim3 grid, const void *q, const void *kc, c
                       const int32_t *sl, void *o, int hkv, int page, int maxb, float *ws, int *cnt, cudaStream_t st);
 int launch_decode_tma(int G, dim3 grid, const void *q, const void *kc, const void *vc, const int32_t *bt,
                       const int32_t *sl, void *o, int hkv, int maxb, float *ws, int *cnt, bool rope, float theta,
-                      cudaStream_t st, int ns);
+                      cudaStream_t st, int ns, const SKView *skv = nullptr, long ldq = 0);
 static int g_attn_tma = [] {
   const char *e = getenv("HX_ATTN_TMA");
   return e ? atoi(e) : 1;
@@ -531,6 +531,37 @@ extern "C" int hx_attn_decode_rope_append(const void *qkv, void *k_cache, void *
   }
   return launch_decode_tma(G, dim3(batch * hkv, splits), qkv, k_cache, v_cache, block_table, seq_lens, o, hkv,
                            max_blocks, ws, cnt, true, theta, as_stream(stream), ns);
+}
+
+extern "C" int hx_attn_decode_rope_append_sk(const float *qkv32, int ld_qkv, const void *gemm_workspace, int k_dim,
+                                             void *k_cache, void *v_cache, const int32_t *block_table,
+                                             const int32_t *seq_lens, void *o, int batch, int hq, int hkv, int hd,
+                                             int page_size, int max_blocks, int max_ctx, float theta, void *workspace,
+                                             size_t workspace_bytes, hx_stream_t stream) {
+  if (batch == 0) return 0;
+  if (!qkv32 || !gemm_workspace || !k_cache || !v_cache || !block_table || !seq_lens || !o || hq % hkv ||
+      ld_qkv < (hq + 2 * hkv) * hd || k_dim <= 0)
+    return HX_ERR_ARG;
+  const int G = hq / hkv;
+  if (hd != 128 || page_size != 64 || !g_attn_tma || !(G == 1 || G == 2 || G == 4 || G == 8 || G == 16))
+    return HX_ERR_UNSUPPORTED;
+  SKView skv;
+  int rc = sk_view_for(batch, (hq + 2 * hkv) * hd, k_dim, gemm_workspace, &skv);
+  if (rc) return rc;
+  int ns = 3;
+  const int splits = tma_decode_splits(batch, hkv, max_ctx, &ns);
+  if (ns == 6) return HX_ERR_UNSUPPORTED;
+  float *ws = nullptr;
+  int *cnt = nullptr;
+  if (splits > 1) {
+    if (!workspace || workspace_bytes < hx_attn_decode_workspace(batch, hq, hkv, hd, max_ctx))
+      return HX_ERR_WORKSPACE;
+    if (batch * hkv > kMaxTickets) return HX_ERR_UNSUPPORTED;
+    cnt = reinterpret_cast<int *>(workspace);
+    ws = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(workspace) + kTicketBytes);
+  }
+  return launch_decode_tma(G, dim3(batch * hkv, splits), qkv32, k_cache, v_cache, block_table, seq_lens, o, hkv,
+                           max_blocks, ws, cnt, true, theta, as_stream(stream), ns, &skv, ld_qkv);
 }
 
 template <typename T, int HD>

@@ -13,6 +13,8 @@
 // kernels in hx_attention.cu.
 #include <cstdlib>
 
+#include <climits>
+
 #include "hx_common.cuh"
 
 namespace hx {
@@ -397,12 +399,65 @@ __device__ __forceinline__ uint32_t sw128_addr(uint32_t base, int r, int col) {
   return base + half * 8192 + r * 128 + ((chunk ^ (r & 7)) << 4) + ((col & 7) << 1);
 }
 
-template <int G, bool ROPE, int NS, int BPI, bool CL>
+// DEF (with ROPE): the QKV projection was a deferred stream-K GEMM
+// (HX_LINEAR_DEFER_REDUCE, fp32 output `q` with row pitch ldq): its split tiles
+// are summed here from the GEMM's partial slots, in CTA order, and rounded to
+// bf16 -- the bits the GEMM's own fix-up would have stored -- so the GEMM ends
+// without its serial fix-up tail. Up to 4 (row, pair) items per thread have
+// their partial loads in flight together.
+template <int G>
+__device__ __forceinline__ void gather_qkv_pairs(const SKView &v, const float *y, long ldy, int b, const int *n,
+                                                 int cnt, float2 *out) {
+  constexpr int NI = 4, MAXC = 8;
+  SkTile ti[NI];
+#pragma unroll
+  for (int j = 0; j < NI; ++j) {
+    out[j] = make_float2(0.f, 0.f);
+    ti[j] = SkTile{0, -1, true};
+    if (j < cnt) {
+      ti[j] = sk_tile(v, n[j] / kSkRows);
+      if (ti[j].whole) out[j] = make_float2(y[(long)b * ldy + n[j]], y[(long)b * ldy + n[j] + 64]);
+    }
+  }
+  for (int base = 0;; base += MAXC) {
+    float2 f[NI][MAXC];
+    bool more = false;
+#pragma unroll
+    for (int j = 0; j < NI; ++j)
+#pragma unroll
+      for (int k = 0; k < MAXC; ++k) {
+        const int cc = j < cnt && !ti[j].whole ? ti[j].c_first + base + k : INT_MAX;
+        if (cc <= ti[j].c_last) {
+          const int tt = n[j] / kSkRows;
+          const int sl = 2 * cc + (sk_start(cc, v.units, v.G) < tt * v.KB ? 1 : 0);
+          const float *src = v.ws + ((size_t)sl * v.BN + b) * kSkRows + n[j] % kSkRows;
+          f[j][k] = make_float2(__ldcg(src), __ldcg(src + 64));
+        }
+      }
+#pragma unroll
+    for (int j = 0; j < NI; ++j) {
+      if (j >= cnt || ti[j].whole) continue;
+#pragma unroll
+      for (int k = 0; k < MAXC; ++k)
+        if (ti[j].c_first + base + k <= ti[j].c_last) {
+          out[j].x += f[j][k].x;
+          out[j].y += f[j][k].y;
+        }
+      more |= ti[j].c_first + base + MAXC <= ti[j].c_last;
+    }
+    if (!more) break;
+  }
+#pragma unroll
+  for (int j = 0; j < NI; ++j)  // the bf16 value the GEMM would have stored
+    out[j] = make_float2(__bfloat162float(__float2bfloat16_rn(out[j].x)), __bfloat162float(__float2bfloat16_rn(out[j].y)));
+}
+
+template <int G, bool ROPE, int NS, int BPI, bool CL, bool DEF = false>
 __global__ void __launch_bounds__(AM_THREADS * BPI)
     attn_decode_tma_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
                            const __nv_bfloat16 *q, const int32_t *bt, const int32_t *seq_lens, __nv_bfloat16 *o,
                            int hkv, int max_blocks, float sl2, float *ws, int *counters, __nv_bfloat16 *kc,
-                           __nv_bfloat16 *vc, float theta) {
+                           __nv_bfloat16 *vc, float theta, SKView skv, long ldq) {
   constexpr int HD = 128, LD = HD + 8, PAGE = 64;
   constexpr uint32_t BLK = PAGE * HD * 2;  // 16 KB per tensor per block
   extern __shared__ __align__(1024) uint8_t smraw[];
@@ -457,7 +512,54 @@ __global__ void __launch_bounds__(AM_THREADS * BPI)
     for (int i = 0; i < pre; ++i) issue(i);
   }
   pdl_wait();
-  if constexpr (ROPE) {
+  if constexpr (DEF) {
+    static_assert(ROPE, "the deferred QKV path is the fused RoPE + KV-append path");
+    const int i = threadIdx.x & 63;
+    const float *y = reinterpret_cast<const float *>(q);
+    const float inv_freq = 1.0f / powf(theta, (float)(2 * i) / 128.0f);
+    float sn, cs;
+    sincosf((float)pos * inv_freq, &sn, &cs);
+    constexpr int STEP = AM_THREADS * BPI / 64;  // q rows handled per pass
+    for (int r0 = threadIdx.x >> 6; r0 < 16; r0 += 4 * STEP) {
+      int n[4], cnt = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int r = r0 + j * STEP;
+        if (r < G) n[cnt++] = (kvh * G + r) * HD + i;
+      }
+      float2 xv[4];
+      gather_qkv_pairs<G>(skv, y, ldq, b, n, cnt, xv);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int r = r0 + j * STEP;
+        if (r >= 16) continue;
+        float y1 = 0.f, y2 = 0.f;
+        if (r < G) {
+          const float2 yy = rope_rot(xv[j].x, xv[j].y, cs, sn);
+          y1 = yy.x;
+          y2 = yy.y;
+        }
+        qs[r * LD + i] = __float2bfloat16_rn(y1);
+        qs[r * LD + i + 64] = __float2bfloat16_rn(y2);
+      }
+    }
+    if (t0 <= pos && pos < t1) {
+      const size_t slot = (((size_t)btb[pos / PAGE] * hkv + kvh) * PAGE + pos % PAGE) * HD;
+      const bool is_k = threadIdx.x < 64;
+      int n[1] = {((is_k ? hq : hq + hkv) + kvh) * HD + i};
+      float2 xv[4];
+      gather_qkv_pairs<G>(skv, y, ldq, b, n, threadIdx.x < 128 ? 1 : 0, xv);
+      if (is_k) {
+        const float2 yy = rope_rot(xv[0].x, xv[0].y, cs, sn);
+        kc[slot + i] = __float2bfloat16_rn(yy.x);
+        kc[slot + i + 64] = __float2bfloat16_rn(yy.y);
+      } else if (threadIdx.x < 128) {
+        vc[slot + i] = __float2bfloat16_rn(xv[0].x);
+        vc[slot + i + 64] = __float2bfloat16_rn(xv[0].y);
+      }
+      fence_proxy_async_global();  // the page is about to be read back by TMA
+    }
+  } else if constexpr (ROPE) {
     // q rows straight from the packed qkv row, rotated here (rotate-half pairs
     // (i, i + 64), same fp32 arithmetic as rope_append_kernel); the CTA whose
     // range holds the new token also rotates its k and appends k, v to the page
@@ -681,23 +783,25 @@ __global__ void __launch_bounds__(AM_THREADS * BPI)
   }
 }
 
-template <int G, bool ROPE, int NS, int BPI, bool CL = false>
+template <int G, bool ROPE, int NS, int BPI, bool CL = false, bool DEF = false>
 static int launch_decode_tma_g(dim3 grid, const CUtensorMap &mk, const CUtensorMap &mv, const void *q,
                                const int32_t *bt, const int32_t *sl, void *o, int hkv, int maxb, float *ws, int *cnt,
-                               void *kc, void *vc, float theta, cudaStream_t st) {
+                               void *kc, void *vc, float theta, cudaStream_t st, const SKView &skv = SKView{},
+                               long ldq = 0) {
   const size_t smem = 1024 + NS * 2 * 16384 + 16 * 136 * 2 + NS * 8 + 16;
+  auto kern = attn_decode_tma_kernel<G, ROPE, NS, BPI, CL, DEF>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(attn_decode_tma_kernel<G, ROPE, NS, BPI, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
   const float sl2 = 1.4426950408889634f / sqrtf(128.f);
   if constexpr (CL)
-    return launch_cluster(attn_decode_tma_kernel<G, ROPE, NS, BPI, CL>, dim3(grid.x * grid.y), dim3(AM_THREADS * BPI),
-                          smem, st, (int)grid.y, mk, mv, (const __nv_bfloat16 *)q, bt, sl, (__nv_bfloat16 *)o, hkv, maxb,
-                          sl2, ws, cnt, (__nv_bfloat16 *)kc, (__nv_bfloat16 *)vc, theta);
-  return launch(attn_decode_tma_kernel<G, ROPE, NS, BPI, CL>, grid, dim3(AM_THREADS * BPI), smem, st, mk, mv, (const __nv_bfloat16 *)q,
-                bt, sl, (__nv_bfloat16 *)o, hkv, maxb, sl2, ws, cnt, (__nv_bfloat16 *)kc, (__nv_bfloat16 *)vc, theta);
+    return launch_cluster(kern, dim3(grid.x * grid.y), dim3(AM_THREADS * BPI), smem, st, (int)grid.y, mk, mv,
+                          (const __nv_bfloat16 *)q, bt, sl, (__nv_bfloat16 *)o, hkv, maxb, sl2, ws, cnt,
+                          (__nv_bfloat16 *)kc, (__nv_bfloat16 *)vc, theta, skv, ldq);
+  return launch(kern, grid, dim3(AM_THREADS * BPI), smem, st, mk, mv, (const __nv_bfloat16 *)q, bt, sl,
+                (__nv_bfloat16 *)o, hkv, maxb, sl2, ws, cnt, (__nv_bfloat16 *)kc, (__nv_bfloat16 *)vc, theta, skv, ldq);
 }
 
 static const int g_attn_cluster = [] {  // split-KV combine over DSMEM clusters (HX_ATTN_CLUSTER=0: workspace)
@@ -709,7 +813,7 @@ static const int g_attn_cluster = [] {  // split-KV combine over DSMEM clusters 
 // new token's k (rotated) and v are appended by the kernel itself.
 int launch_decode_tma(int G, dim3 grid, const void *q, const void *kc, const void *vc, const int32_t *bt,
                       const int32_t *sl, void *o, int hkv, int maxb, float *ws, int *cnt, bool rope, float theta,
-                      cudaStream_t st, int ns) {
+                      cudaStream_t st, int ns, const SKView *skv, long ldq) {
   CUtensorMap mk, mv;
   // the pool size is not part of the C-ABI: declare 2^28 rows (64 GB of K); only
   // rows of blocks named by the block table are ever addressed
@@ -718,6 +822,24 @@ int launch_decode_tma(int G, dim3 grid, const void *q, const void *kc, const voi
   if (!rc) rc = make_tma_bf16_sw128(&mv, vc, rows, 128, 128, 64);
   if (rc) return rc;
   void *k = const_cast<void *>(kc), *v = const_cast<void *>(vc);
+  if (skv) {  // deferred QKV (fused RoPE + KV append), 3-deep ring, 1 block per iteration
+    if (!rope || ns == 6) return HX_ERR_UNSUPPORTED;
+#define HX_TMA_DEF(GG)                                                                                              \
+  if (grid.y >= 2 && grid.y <= 8 && g_attn_cluster)                                                               \
+    return launch_decode_tma_g<GG, true, 3, 1, true, true>(grid, mk, mv, q, bt, sl, o, hkv, maxb, ws, cnt, k, v, theta, \
+                                                           st, *skv, ldq);                                          \
+  return launch_decode_tma_g<GG, true, 3, 1, false, true>(grid, mk, mv, q, bt, sl, o, hkv, maxb, ws, cnt, k, v, theta, \
+                                                          st, *skv, ldq)
+    switch (G) {
+      case 1: HX_TMA_DEF(1);
+      case 2: HX_TMA_DEF(2);
+      case 4: HX_TMA_DEF(4);
+      case 8: HX_TMA_DEF(8);
+      case 16: HX_TMA_DEF(16);
+    }
+#undef HX_TMA_DEF
+    return HX_ERR_UNSUPPORTED;
+  }
 #define HX_TMA_G(GG)                                                                                               \
   if (ns == 6)                                                                                                     \
     return rope ? launch_decode_tma_g<GG, true, 6, 2>(grid, mk, mv, q, bt, sl, o, hkv, maxb, ws, cnt, k, v, theta, st) \

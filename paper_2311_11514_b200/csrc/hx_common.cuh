@@ -368,4 +368,101 @@ __host__ __device__ constexpr uint32_t umma_idesc_bf16(int M, int N) {
          ((uint32_t)(M >> 4) << 24);
 }
 
+// ---------------------------------------------------------------- stream-K partition
+// The persistent decode GEMM (hx_gemm.cu) splits units = (128-row tile, 64-wide
+// K block) evenly over G CTAs: CTA c owns [sk_start(c), sk_start(c + 1)). A
+// tile covered by one CTA is written whole; a tile split across CTAs leaves
+// fp32 partials in workspace slots 2c (c's first segment) / 2c + 1 (its last),
+// laid out [slot][token][128 rows]. Consumers of a deferred GEMM
+// (HX_LINEAR_DEFER_REDUCE) sum those partials in CTA order -- the same
+// arithmetic as the in-kernel fix-up, so the bits are identical.
+constexpr int kSkRows = 128;
+
+__device__ __forceinline__ int sk_start(int c, int units, int G) { return (int)((unsigned)(c * units) / (unsigned)G); }
+
+// first CTA whose range contains unit u
+__device__ __forceinline__ int sk_owner(int u, int units, int G) {
+  int c = (int)((unsigned)(u * G) / (unsigned)units);
+  while (c + 1 < G && sk_start(c + 1, units, G) <= u) ++c;
+  while (c > 0 && sk_start(c, units, G) > u) --c;
+  return c;
+}
+
+struct SKView {
+  const float *ws;  // partial slots (workspace + kTicketBytes)
+  int units, KB, G, BN;
+};
+
+// host: the view of hx_linear(n_tok, n_out, k_dim) deferred into `workspace`
+int sk_view_for(int n_tok, int n_out, int k_dim, const void *workspace, SKView *v);
+
+struct SkTile {
+  int c_first, c_last;
+  bool whole;
+};
+
+__device__ __forceinline__ SkTile sk_tile(const SKView &v, int tt) {
+  SkTile t;
+  t.c_first = sk_owner(tt * v.KB, v.units, v.G);
+  t.c_last = sk_owner((tt + 1) * v.KB - 1, v.units, v.G);
+  t.whole = t.c_first == t.c_last && sk_start(t.c_first, v.units, v.G) <= tt * v.KB &&
+            (t.c_first + 1 >= v.G ? v.units : sk_start(t.c_first + 1, v.units, v.G)) >= (tt + 1) * v.KB;
+  return t;
+}
+
+__device__ __forceinline__ float4 sk_gather4(const SKView &v, const float *y, long ldy, int t, int n) {
+  const int tt = n / kSkRows, r = n % kSkRows;
+  const SkTile ti = sk_tile(v, tt);
+  if (ti.whole) return *reinterpret_cast<const float4 *>(y + (long)t * ldy + n);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  constexpr int MAXC = 8;  // all contributors' loads in flight together
+  for (int cb = ti.c_first; cb <= ti.c_last; cb += MAXC) {
+    float4 f[MAXC];
+#pragma unroll
+    for (int i = 0; i < MAXC; ++i) {
+      const int cc = cb + i;
+      if (cc <= ti.c_last) {
+        const int sl = 2 * cc + (sk_start(cc, v.units, v.G) < tt * v.KB ? 1 : 0);
+        f[i] = __ldcg(reinterpret_cast<const float4 *>(v.ws + ((size_t)sl * v.BN + t) * kSkRows + r));
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < MAXC; ++i) {
+      if (cb + i <= ti.c_last) {
+        acc.x += f[i].x; acc.y += f[i].y; acc.z += f[i].z; acc.w += f[i].w;
+      }
+    }
+  }
+  return acc;
+}
+
+// features n and n + 64 of token t (one 128-row tile: a RoPE rotate-half pair)
+__device__ __forceinline__ float2 sk_gather_pair(const SKView &v, const float *y, long ldy, int t, int n) {
+  const int tt = n / kSkRows, r = n % kSkRows;
+  const SkTile ti = sk_tile(v, tt);
+  if (ti.whole) return make_float2(y[(long)t * ldy + n], y[(long)t * ldy + n + 64]);
+  float2 acc = make_float2(0.f, 0.f);
+  constexpr int MAXC = 8;
+  for (int cb = ti.c_first; cb <= ti.c_last; cb += MAXC) {
+    float2 f[MAXC];
+#pragma unroll
+    for (int i = 0; i < MAXC; ++i) {
+      const int cc = cb + i;
+      if (cc <= ti.c_last) {
+        const int sl = 2 * cc + (sk_start(cc, v.units, v.G) < tt * v.KB ? 1 : 0);
+        const float *src = v.ws + ((size_t)sl * v.BN + t) * kSkRows + r;
+        f[i] = make_float2(__ldcg(src), __ldcg(src + 64));
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < MAXC; ++i) {
+      if (cb + i <= ti.c_last) {
+        acc.x += f[i].x;
+        acc.y += f[i].y;
+      }
+    }
+  }
+  return acc;
+}
+
 }  // namespace hx

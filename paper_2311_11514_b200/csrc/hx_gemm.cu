@@ -460,15 +460,6 @@ __device__ __forceinline__ void emit_decode(const OutDesc od, const EpiArgs &epi
   }
 }
 
-__device__ __forceinline__ int sk_start(int c, int units, int G) { return (int)((unsigned)(c * units) / (unsigned)G); }
-
-// first CTA whose range contains unit u
-__device__ __forceinline__ int sk_owner(int u, int units, int G) {
-  int c = (int)((unsigned)(u * G) / (unsigned)units);
-  while (c + 1 < G && sk_start(c + 1, units, G) <= u) ++c;
-  while (c > 0 && sk_start(c, units, G) > u) --c;
-  return c;
-}
 
 template <int BN, int STAGES, bool FUSED>
 __global__ void __launch_bounds__(192, 2)
@@ -681,40 +672,6 @@ __global__ void __launch_bounds__(192, 2)
 // This moves the split-K reduction (two dependent L2 round trips under a
 // saturated memory system) off the GEMM's critical tail into a kernel that
 // reads its input anyway.
-struct SKView {
-  const float *ws;
-  int units, KB, G, BN;
-};
-
-__device__ __forceinline__ float4 sk_gather4(const SKView &v, const float *y, long ldy, int t, int n) {
-  const int tt = n / BM, r = n % BM;
-  const int c_first = sk_owner(tt * v.KB, v.units, v.G);
-  const int c_last = sk_owner((tt + 1) * v.KB - 1, v.units, v.G);
-  const bool whole = c_first == c_last && sk_start(c_first, v.units, v.G) <= tt * v.KB &&
-                     (c_first + 1 >= v.G ? v.units : sk_start(c_first + 1, v.units, v.G)) >= (tt + 1) * v.KB;
-  if (whole) return *reinterpret_cast<const float4 *>(y + (long)t * ldy + n);
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  constexpr int MAXC = 8;  // all contributors' loads in flight together
-  for (int cb = c_first; cb <= c_last; cb += MAXC) {
-    float4 f[MAXC];
-#pragma unroll
-    for (int i = 0; i < MAXC; ++i) {
-      const int cc = cb + i;
-      if (cc <= c_last) {
-        const int sl = 2 * cc + (sk_start(cc, v.units, v.G) < tt * v.KB ? 1 : 0);
-        f[i] = __ldcg(reinterpret_cast<const float4 *>(v.ws + ((size_t)sl * v.BN + t) * BM + r));
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < MAXC; ++i) {
-      if (cb + i <= c_last) {
-        acc.x += f[i].x; acc.y += f[i].y; acc.z += f[i].z; acc.w += f[i].w;
-      }
-    }
-  }
-  return acc;
-}
-
 constexpr int SK_CL = 4;
 
 template <typename TO>
@@ -1021,6 +978,20 @@ static int launch_sk(const CUtensorMap &mw, const CUtensorMap &mx, const SKArgs 
   }
   return launch(gemm_streamk_kernel<BN, STAGES, FUSED>, dim3(sk_grid(p.units)), dim3(192), smem, st, mw, mx, p);
 }
+
+namespace hx {
+// The deferred-reduction view of hx_linear(n_tok, n_out, k_dim) with workspace ws.
+int sk_view_for(int n_tok, int n_out, int k_dim, const void *workspace, SKView *v) {
+  Plan pl = plan_gemm(n_tok, n_out, k_dim);
+  if (!pl.decode) return HX_ERR_UNSUPPORTED;
+  v->ws = reinterpret_cast<const float *>(reinterpret_cast<const uint8_t *>(workspace) + kTicketBytes);
+  v->KB = (k_dim + BK - 1) / BK;
+  v->units = pl.tiles * v->KB;
+  v->G = sk_grid(v->units);
+  v->BN = pl.bn;
+  return 0;
+}
+}  // namespace hx
 
 extern "C" int hx_splitk_residual_rmsnorm(float *x, const float *y, int ldy, const void *workspace, int n_tok,
                                           int n_out, int k_dim, const float *gain, void *out, int out_dtype,

@@ -253,6 +253,10 @@ class RankExecutor:
         self._peer_now = False
         self._decode_now = False
         self.attn_ws = torch.zeros(max(self.attn_ws_bytes, 256) // 4 + 64, dtype=torch.int32, device=dev)
+        # decode QKV GEMM without its split-K fix-up tail: partial tiles are reduced
+        # in the attention prologue (bit-identical); HX_DEFER_QKV=0 disables
+        self.defer_qkv = self.rope_in_attn and os.environ.get("HX_DEFER_QKV", "1") != "0"
+        self.qkv32 = z(batch, self.qkv_n, dt=torch.float32) if self.defer_qkv else None
         # tcgen05 prefill attention (default; HX_PREFILL_TC=0 selects the mma.sync
         # kernel): needs V transposed per (sequence, kv head) -- a prefill-only scratch
         self.tc_prefill = (os.environ.get("HX_PREFILL_TC", "1") == "1" and dtype == torch.bfloat16
@@ -289,7 +293,11 @@ class RankExecutor:
             k.rmsnorm(self.x, lw["ln_attn"], self.h, n_tok, cfg.rms_eps)
         kc, vc = self.kv.k[li], self.kv.v[li]
         pf = self._l2pf(prefill_len)
-        if self.rope_in_attn and not prefill_len:  # decode: RoPE + KV append inside the attention kernel
+        if self.defer_qkv and not prefill_len and n_tok <= 64:  # decode: split-K reduced by the attention kernel
+            k.linear(lw["wqkv"], self.h, self.qkv32, n_tok, self.lin_ws, defer_reduce=True, **pf)
+            k.attn_decode_rope_append_sk(self.qkv32, self.lin_ws, cfg.hidden_dim, kc, vc, self.bt, self.sl, self.attn,
+                                         n_tok, self.hq, self.hkv, self.hd, self.max_ctx, cfg.rope_theta, self.attn_ws)
+        elif self.rope_in_attn and not prefill_len:  # decode: RoPE + KV append inside the attention kernel
             k.linear(lw["wqkv"], self.h, self.qkv, n_tok, self.lin_ws, **pf)
             k.attn_decode_rope_append(self.qkv, kc, vc, self.bt, self.sl, self.attn, n_tok,
                                       self.hq, self.hkv, self.hd, self.max_ctx, cfg.rope_theta, self.attn_ws)

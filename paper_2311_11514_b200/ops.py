@@ -66,6 +66,8 @@ _SIGS = {
     "hx_attn_decode_workspace": ([_I, _I, _I, _I, _I], _SZ),
     "hx_attn_decode_rope_append": ([_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _F, _P, _SZ, _P], _I),
     "hx_attn_prefill": ([_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P], _I),
+    "hx_attn_decode_rope_append_sk": ([_P, _I, _P, _I, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _F, _P, _SZ,
+                                       _P], _I),
     "hx_advance": ([_P, _I, _I, _P], _I),
     "hx_argmax_partial": ([_P, _P, _I, _I, _I, _I, _P], _I),
     "hx_argmax_finalize": ([_P, _P, _P, _P, _I, _I, _I, _P], _I),
@@ -306,6 +308,18 @@ def attn_decode_rope_append(qkv, k_cache, v_cache, block_table, seq_lens, o, bat
                                              block_table.shape[1], max_ctx, theta, _p(ws),
                                              0 if ws is None else ws.numel() * ws.element_size(), _stream()),
            "hx_attn_decode_rope_append")
+
+
+def attn_decode_rope_append_sk(qkv32, gemm_ws, k_dim, k_cache, v_cache, block_table, seq_lens, o, batch, hq, hkv,
+                               hd, max_ctx, theta, workspace=None):
+    """hx_attn_decode_rope_append after a deferred QKV GEMM (linear(..., defer_reduce=True)
+    into fp32 qkv32 with workspace gemm_ws): the split tiles are reduced in the prologue."""
+    ws = workspace
+    _check(load().hx_attn_decode_rope_append_sk(_p(qkv32), qkv32.shape[-1], _p(gemm_ws), k_dim, _p(k_cache),
+                                                _p(v_cache), _p(block_table), _p(seq_lens), _p(o), batch, hq, hkv,
+                                                hd, k_cache.shape[2], block_table.shape[1], max_ctx, theta, _p(ws),
+                                                0 if ws is None else ws.numel() * ws.element_size(), _stream()),
+           "hx_attn_decode_rope_append_sk")
 
 
 def attn_prefill(q, k_cache, v_cache, block_table, seq_lens, o, batch, s, hq, hkv, hd):

@@ -450,3 +450,40 @@ def test_prefill_attention_tcgen05(b, s, hq, hkv):
     assert torch.equal(vt.view(b, hkv, hd, s).float(), v.permute(0, 2, 3, 1))
     torch.cuda.synchronize()
     assert rel_err(o, want) < 2e-2
+
+
+@pytest.mark.parametrize("b,hq,hkv,hidden,ctx", [(8, 32, 32, 4096, 575), (32, 16, 2, 8192, 1100), (8, 20, 20, 5120, 600),
+                                                (32, 32, 4, 8192, 700), (4, 8, 8, 2048, 130)])
+def test_deferred_qkv_into_attention_bit_identical(b, hq, hkv, hidden, ctx):
+    """QKV as a deferred stream-K GEMM (fp32 partial slots, no fix-up) whose split
+    tiles the attention prologue reduces (hx_attn_decode_rope_append_sk) ==
+    hx_linear (bf16 qkv, in-kernel fix-up) + hx_attn_decode_rope_append, bit for
+    bit: attention output and the appended K/V page slots. Shapes: 7B, 70B TP=4,
+    13B TP=2, 70B TP=2, small."""
+    dt, hd, page = torch.bfloat16, 128, 64
+    kc, vc, bt, g = _paged_setup(dt, b, hq, hkv, hd, page, ctx + 1)
+    n = (hq + 2 * hkv) * hd
+    hist = torch.randn(b * ctx, n, device=DEV, generator=g).to(dt)
+    seq = torch.zeros(b, dtype=torch.int32, device=DEV)
+    ops.rope_kv_append(hist, torch.empty(b * ctx, hq * hd, device=DEV, dtype=dt), kc, vc, bt, seq, b * ctx, ctx,
+                       hq, hkv, hd, 10000.0)
+    seq.copy_(torch.tensor([max(1, ctx - 61 * i) for i in range(b)], dtype=torch.int32))
+    w = ops.PackedWeight((torch.randn(n, hidden, device=DEV, generator=g) * 0.02).bfloat16())
+    x = torch.randn(b, hidden, device=DEV, generator=g).bfloat16()
+    lin_ws = torch.zeros(ops.linear_workspace(dt, b, n, hidden) // 4 + 64, dtype=torch.int32, device=DEV)
+    attn_ws = torch.zeros(ops.attn_decode_workspace(b, hq, hkv, hd, ctx + 1) // 4 + 64, dtype=torch.int32,
+                          device=DEV)
+    k2, v2 = kc.clone(), vc.clone()
+    qkv = torch.empty(b, n, device=DEV, dtype=dt)
+    o_ref = torch.empty(b, hq * hd, device=DEV, dtype=dt)
+    ops.linear(w, x, qkv, b, lin_ws)
+    ops.attn_decode_rope_append(qkv, kc, vc, bt, seq, o_ref, b, hq, hkv, hd, ctx + 1, 10000.0, attn_ws)
+    qkv32 = torch.full((b, n), float("nan"), device=DEV)
+    o_def = torch.empty_like(o_ref)
+    for _ in range(2):   # the second call reuses the re-armed tickets
+        ops.linear(w, x, qkv32, b, lin_ws, defer_reduce=True)
+        ops.attn_decode_rope_append_sk(qkv32, lin_ws, hidden, k2, v2, bt, seq, o_def, b, hq, hkv, hd, ctx + 1,
+                                       10000.0, attn_ws)
+        torch.cuda.synchronize()
+        assert torch.equal(k2, kc) and torch.equal(v2, vc)
+        assert torch.equal(o_def, o_ref)
