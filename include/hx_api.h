@@ -171,6 +171,17 @@ int hx_tp_allreduce_push_residual_rmsnorm(float *x, const float *own_part, float
                                           int rank, int tp, int max_tok, int *state,
                                           const float *gain, void *out, int out_dtype, int n_tok,
                                           int hidden, float eps, hx_stream_t stream);
+/* _ex variants: payload_dtype HX_F32 (the calls above) or HX_BF16 -- each
+ * partial row is rounded to bf16 once (on every rank, its own included) and
+ * summed in fp32 in rank order: half the NVLink bytes, all ranks bitwise
+ * identical; inbox halfwords armed with the bf16 sentinel 0x8000. hidden must be
+ * a multiple of 32 for bf16 (16 for fp32). */
+size_t hx_tp_inbox_bytes_ex(int tp, int max_tok, int hidden, int payload_dtype);
+int hx_tp_inbox_init_ex(void *inbox, int tp, int max_tok, int hidden, int payload_dtype, hx_stream_t stream);
+int hx_tp_allreduce_push_residual_rmsnorm_ex(float *x, const float *own_part, void *const *inboxes, int rank,
+                                             int tp, int max_tok, int *state, const float *gain, void *out,
+                                             int out_dtype, int n_tok, int hidden, float eps, int payload_dtype,
+                                             hx_stream_t stream);
 
 /* ---- Inter-stage reshard over NVLink P2P (decode hand-off and token return).
  * Replaces the leader send + broadcast of PAPER.md:197 (modelled by

@@ -145,12 +145,55 @@ __device__ __forceinline__ uint4 ld_volatile_u4(const void *p) {
 __device__ __forceinline__ bool has_sentinel(const uint4 &v) {
   return v.x == kSentinel || v.y == kSentinel || v.z == kSentinel || v.w == kSentinel;
 }
-__device__ __forceinline__ float4 sanitize(float4 v) {  // -0.0 -> +0.0 (bitwise), value-preserving
-  v.x += 0.0f; v.y += 0.0f; v.z += 0.0f; v.w += 0.0f;
-  return v;
-}
 
-template <typename TO>
+// bf16 payload (PL = __nv_bfloat16): each partial is rounded to bf16 once
+// (every rank, its own partial included, so all ranks sum identical values in
+// rank order, accumulating in fp32): half the NVLink bytes of the fp32 payload.
+// Inbox halfwords are armed with the bf16 sentinel 0x8000 (-0.0), pushed -0.0 is
+// sent as +0.0.
+template <typename PL>
+struct ArPayload;
+template <>
+struct ArPayload<float> {
+  static constexpr int V = 4;  // elements per 16-byte vector
+  __device__ static bool armed(const uint4 &u) { return has_sentinel(u); }
+  __device__ static uint4 sentinel() { return make_uint4(kSentinel, kSentinel, kSentinel, kSentinel); }
+  __device__ static uint4 pack(const float *v) {  // -0.0 -> +0.0 (bitwise), value-preserving
+    return make_uint4(__float_as_uint(v[0] + 0.0f), __float_as_uint(v[1] + 0.0f), __float_as_uint(v[2] + 0.0f),
+                      __float_as_uint(v[3] + 0.0f));
+  }
+  __device__ static void unpack(const uint4 &u, float *v) {
+    v[0] = __uint_as_float(u.x); v[1] = __uint_as_float(u.y); v[2] = __uint_as_float(u.z); v[3] = __uint_as_float(u.w);
+  }
+};
+template <>
+struct ArPayload<__nv_bfloat16> {
+  static constexpr int V = 8;
+  static constexpr uint32_t S2 = 0x80008000u;
+  __device__ static bool has16(uint32_t w) { return (w & 0xFFFFu) == 0x8000u || (w >> 16) == 0x8000u; }
+  __device__ static bool armed(const uint4 &u) { return has16(u.x) || has16(u.y) || has16(u.z) || has16(u.w); }
+  __device__ static uint4 sentinel() { return make_uint4(S2, S2, S2, S2); }
+  __device__ static uint32_t pk2(float a, float b) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    uint32_t w = *reinterpret_cast<uint32_t *>(&h);
+    if ((w & 0xFFFFu) == 0x8000u) w &= 0xFFFF0000u;  // -0.0 -> +0.0
+    if ((w >> 16) == 0x8000u) w &= 0x0000FFFFu;
+    return w;
+  }
+  __device__ static uint4 pack(const float *v) {
+    return make_uint4(pk2(v[0], v[1]), pk2(v[2], v[3]), pk2(v[4], v[5]), pk2(v[6], v[7]));
+  }
+  __device__ static void unpack(const uint4 &u, float *v) {
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v[2 * i] = __uint_as_float(w[i] << 16);
+      v[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+    }
+  }
+};
+
+template <typename TO, typename PL>
 __global__ void __launch_bounds__(256)
     tp_ar_push_rmsnorm_kernel(float *x, const float *own, ArInbox ib, int rank, int tp, int max_tok, int *state,
                               const float *gain, TO *out, int hidden, float eps) {
@@ -161,58 +204,70 @@ __global__ void __launch_bounds__(256)
   const int t = blockIdx.x / AR_CL;
   const int per = hidden / AR_CL, base = (int)cr * per;
   const size_t row = (size_t)hidden;
-  constexpr int MAXV = 2;  // hidden <= AR_CL * 2 * 4 * 256 = 8192
-  float4 gv[MAXV];
-#pragma unroll
-  for (int i = 0; i < MAXV; ++i) {  // the gain is a weight: fetch it before the wait
-    const int n = base + (i * 256 + threadIdx.x) * 4;
-    if (out && n < base + per) gv[i] = __ldg(reinterpret_cast<const float4 *>(gain + n));
-  }
+  if (out && threadIdx.x < per / 32)   // the gain is a weight: pull this CTA's slice into L1 before the wait
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(gain + base + threadIdx.x * 32));
   pdl_wait();  // this rank's partial (previous kernel) is complete
   const int call = *(volatile int *)state;
   const int buf = call & 1;
-  float *mine = ib.box[rank];
-  float4 p[MAXV];
+  // inbox element index of (buffer, sender r, token t, feature n); payload elements of PL
+  constexpr int V = ArPayload<PL>::V;   // features per 16-byte vector
+  constexpr int NV = 2048 / (256 * V);  // vectors per thread: <= 2048 features per CTA (hidden <= 8192)
+  PL *mine = reinterpret_cast<PL *>(ib.box[rank]);
+  auto at = [&](PL *box, int r, int n) { return box + (((size_t)buf * tp + r) * max_tok + t) * row + n; };
+  float p[NV][V];
   // 1. push my partial slice of row t to every peer (remote stores, fire and forget)
 #pragma unroll
-  for (int i = 0; i < MAXV; ++i) {
-    const int n = base + (i * 256 + threadIdx.x) * 4;
+  for (int i = 0; i < NV; ++i) {
+    const int n = base + (i * 256 + threadIdx.x) * V;
     if (n >= base + per) continue;
-    p[i] = sanitize(__ldcs(reinterpret_cast<const float4 *>(own + (size_t)t * row + n)));
+#pragma unroll
+    for (int j = 0; j < V; j += 4) {
+      const float4 f = __ldcs(reinterpret_cast<const float4 *>(own + (size_t)t * row + n + j));
+      p[i][j] = f.x; p[i][j + 1] = f.y; p[i][j + 2] = f.z; p[i][j + 3] = f.w;
+    }
+    const uint4 w = ArPayload<PL>::pack(p[i]);
+    ArPayload<PL>::unpack(w, p[i]);  // this rank sums exactly the values its peers receive
     for (int r = 0; r < tp; ++r)
-      if (r != rank)
-        *reinterpret_cast<float4 *>(ib.box[r] + (((size_t)buf * tp + rank) * max_tok + t) * row + n) = p[i];
+      if (r != rank) *reinterpret_cast<uint4 *>(at(reinterpret_cast<PL *>(ib.box[r]), rank, n)) = w;
   }
   // 2. poll my inbox for every peer's slice, re-arm it in place, sum in rank order
   //    (bitwise identical on all ranks), residual
-  const float4 s4 = make_float4(__uint_as_float(kSentinel), __uint_as_float(kSentinel), __uint_as_float(kSentinel),
-                                __uint_as_float(kSentinel));
+  const uint4 s4 = ArPayload<PL>::sentinel();
   float ss = 0.f;
-  float4 v[MAXV];
+  float v[NV][V];
 #pragma unroll
-  for (int i = 0; i < MAXV; ++i) {
-    const int n = base + (i * 256 + threadIdx.x) * 4;
+  for (int i = 0; i < NV; ++i) {
+    const int n = base + (i * 256 + threadIdx.x) * V;
     if (n >= base + per) continue;
-    float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+    float sum[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) sum[j] = 0.f;
     for (int r = 0; r < tp; ++r) {
-      float4 q = p[i];
+      float q[V];
       if (r != rank) {
-        float *src = mine + (((size_t)buf * tp + r) * max_tok + t) * row + n;
+        PL *src = at(mine, r, n);
         uint4 u = ld_volatile_u4(src);
-        for (uint32_t spins = 0; has_sentinel(u); ++spins) {
+        for (uint32_t spins = 0; ArPayload<PL>::armed(u); ++spins) {
           if (spins > (1u << 26)) __trap();  // a peer never arrived: fail loudly, never hang
           u = ld_volatile_u4(src);
         }
-        *reinterpret_cast<float4 *>(src) = s4;
-        q = make_float4(__uint_as_float(u.x), __uint_as_float(u.y), __uint_as_float(u.z), __uint_as_float(u.w));
+        *reinterpret_cast<uint4 *>(src) = s4;
+        ArPayload<PL>::unpack(u, q);
+      } else {
+#pragma unroll
+        for (int j = 0; j < V; ++j) q[j] = p[i][j];
       }
-      sum.x += q.x; sum.y += q.y; sum.z += q.z; sum.w += q.w;
+#pragma unroll
+      for (int j = 0; j < V; ++j) sum[j] += q[j];
     }
-    float4 acc = *reinterpret_cast<const float4 *>(x + (size_t)t * row + n);
-    acc.x += sum.x; acc.y += sum.y; acc.z += sum.z; acc.w += sum.w;
-    *reinterpret_cast<float4 *>(x + (size_t)t * row + n) = acc;
-    v[i] = acc;
-    ss += acc.x * acc.x + acc.y * acc.y + acc.z * acc.z + acc.w * acc.w;
+#pragma unroll
+    for (int j = 0; j < V; j += 4) {
+      float4 acc = *reinterpret_cast<const float4 *>(x + (size_t)t * row + n + j);
+      acc.x += sum[j]; acc.y += sum[j + 1]; acc.z += sum[j + 2]; acc.w += sum[j + 3];
+      *reinterpret_cast<float4 *>(x + (size_t)t * row + n + j) = acc;
+      v[i][j] = acc.x; v[i][j + 1] = acc.y; v[i][j + 2] = acc.z; v[i][j + 3] = acc.w;
+      ss += acc.x * acc.x + acc.y * acc.y + acc.z * acc.z + acc.w * acc.w;
+    }
   }
   // 3. RMSNorm across the cluster (DSMEM), same summation order in every CTA
   if (out) {
@@ -231,11 +286,15 @@ __global__ void __launch_bounds__(256)
     const float inv = 1.0f / sqrtf(tot / (float)hidden + eps);
     TO *o = out + (size_t)t * row;
 #pragma unroll
-    for (int i = 0; i < MAXV; ++i) {
-      const int n = base + (i * 256 + threadIdx.x) * 4;
+    for (int i = 0; i < NV; ++i) {
+      const int n = base + (i * 256 + threadIdx.x) * V;
       if (n >= base + per) continue;
-      const float4 g = gv[i];
-      store4(o + n, (v[i].x * inv) * g.x, (v[i].y * inv) * g.y, (v[i].z * inv) * g.z, (v[i].w * inv) * g.w);
+#pragma unroll
+      for (int j = 0; j < V; j += 4) {
+        const float4 g = __ldg(reinterpret_cast<const float4 *>(gain + n + j));
+        store4(o + n + j, (v[i][j] * inv) * g.x, (v[i][j + 1] * inv) * g.y, (v[i][j + 2] * inv) * g.z,
+               (v[i][j + 3] * inv) * g.w);
+      }
     }
   }
   __syncthreads();
@@ -306,36 +365,64 @@ extern "C" int hx_tp_allreduce_residual_rmsnorm(float *x, const float *const *pa
                 site_state, gain, (float *)out, hidden, eps);
 }
 
+extern "C" size_t hx_tp_inbox_bytes_ex(int tp, int max_tok, int hidden, int payload_dtype) {
+  return (size_t)2 * tp * max_tok * hidden * (payload_dtype == HX_BF16 ? 2 : 4);
+}
+
 extern "C" size_t hx_tp_inbox_bytes(int tp, int max_tok, int hidden) {
-  return (size_t)2 * tp * max_tok * hidden * sizeof(float);
+  return hx_tp_inbox_bytes_ex(tp, max_tok, hidden, HX_F32);
+}
+
+extern "C" int hx_tp_inbox_init_ex(void *inbox, int tp, int max_tok, int hidden, int payload_dtype,
+                                   hx_stream_t stream) {
+  if (!inbox || tp < 1 || max_tok < 1 || hidden < 1) return HX_ERR_ARG;
+  // load the kernels before any rank spins in them (lazy loading, see hx_handoff_inbox_init)
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, tp_ar_push_rmsnorm_kernel<float, float>);
+  cudaFuncGetAttributes(&fa, tp_ar_push_rmsnorm_kernel<__nv_bfloat16, float>);
+  cudaFuncGetAttributes(&fa, tp_ar_push_rmsnorm_kernel<float, __nv_bfloat16>);
+  cudaFuncGetAttributes(&fa, tp_ar_push_rmsnorm_kernel<__nv_bfloat16, __nv_bfloat16>);
+  const size_t n = hx_tp_inbox_bytes_ex(tp, max_tok, hidden, payload_dtype) / 4;
+  fill_u32_kernel<<<296, 256, 0, as_stream(stream)>>>((uint32_t *)inbox, n,
+                                                       payload_dtype == HX_BF16 ? 0x80008000u : kSentinel);
+  return launch_status();
 }
 
 extern "C" int hx_tp_inbox_init(void *inbox, int tp, int max_tok, int hidden, hx_stream_t stream) {
-  if (!inbox || tp < 1 || max_tok < 1 || hidden < 1) return HX_ERR_ARG;
-  // load the kernel before any rank spins in it (lazy loading, see hx_handoff_inbox_init)
-  cudaFuncAttributes fa;
-  cudaFuncGetAttributes(&fa, tp_ar_push_rmsnorm_kernel<float>);
-  cudaFuncGetAttributes(&fa, tp_ar_push_rmsnorm_kernel<__nv_bfloat16>);
-  const size_t n = hx_tp_inbox_bytes(tp, max_tok, hidden) / 4;
-  fill_u32_kernel<<<296, 256, 0, as_stream(stream)>>>((uint32_t *)inbox, n, kSentinel);
-  return launch_status();
+  return hx_tp_inbox_init_ex(inbox, tp, max_tok, hidden, HX_F32, stream);
+}
+
+extern "C" int hx_tp_allreduce_push_residual_rmsnorm_ex(float *x, const float *own_part, void *const *inboxes, int rank,
+                                                        int tp, int max_tok, int *state, const float *gain, void *out,
+                                                        int out_dtype, int n_tok, int hidden, float eps,
+                                                        int payload_dtype, hx_stream_t stream) {
+  if (n_tok == 0) return 0;
+  const int V = payload_dtype == HX_BF16 ? 8 : 4;
+  if (!x || !own_part || !inboxes || !state || tp < 1 || tp > kMaxTP || rank < 0 || rank >= tp ||
+      n_tok > max_tok || hidden % (V * AR_CL) || hidden > 8192 || (out && !gain) ||
+      (payload_dtype != HX_F32 && payload_dtype != HX_BF16))
+    return HX_ERR_ARG;
+  ArInbox ib{};
+  for (int r = 0; r < tp; ++r) ib.box[r] = reinterpret_cast<float *>(inboxes[r]);
+  cudaStream_t st = as_stream(stream);
+  const dim3 grid(n_tok * AR_CL);
+#define HX_AR(TO, PL)                                                                                              \
+  return launch_cluster(tp_ar_push_rmsnorm_kernel<TO, PL>, grid, dim3(256), 0, st, AR_CL, x, own_part, ib, rank, tp, \
+                        max_tok, state, gain, (TO *)out, hidden, eps)
+  if (payload_dtype == HX_BF16) {
+    if (out_dtype == HX_BF16) HX_AR(__nv_bfloat16, __nv_bfloat16);
+    HX_AR(float, __nv_bfloat16);
+  }
+  if (out_dtype == HX_BF16) HX_AR(__nv_bfloat16, float);
+  HX_AR(float, float);
+#undef HX_AR
 }
 
 extern "C" int hx_tp_allreduce_push_residual_rmsnorm(float *x, const float *own_part, float *const *inboxes, int rank,
                                                      int tp, int max_tok, int *state, const float *gain, void *out,
                                                      int out_dtype, int n_tok, int hidden, float eps,
                                                      hx_stream_t stream) {
-  if (n_tok == 0) return 0;
-  if (!x || !own_part || !inboxes || !state || tp < 1 || tp > kMaxTP || rank < 0 || rank >= tp ||
-      n_tok > max_tok || hidden % (4 * AR_CL) || hidden > 8192 || (out && !gain))
-    return HX_ERR_ARG;
-  ArInbox ib{};
-  for (int r = 0; r < tp; ++r) ib.box[r] = inboxes[r];
-  cudaStream_t st = as_stream(stream);
-  const dim3 grid(n_tok * AR_CL);
-  if (out_dtype == HX_BF16)
-    return launch_cluster(tp_ar_push_rmsnorm_kernel<__nv_bfloat16>, grid, dim3(256), 0, st, AR_CL, x, own_part, ib,
-                          rank, tp, max_tok, state, gain, (__nv_bfloat16 *)out, hidden, eps);
-  return launch_cluster(tp_ar_push_rmsnorm_kernel<float>, grid, dim3(256), 0, st, AR_CL, x, own_part, ib, rank, tp,
-                        max_tok, state, gain, (float *)out, hidden, eps);
+  return hx_tp_allreduce_push_residual_rmsnorm_ex(x, own_part, reinterpret_cast<void *const *>(inboxes), rank, tp,
+                                                  max_tok, state, gain, out, out_dtype, n_tok, hidden, eps, HX_F32,
+                                                  stream);
 }

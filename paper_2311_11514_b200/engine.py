@@ -612,17 +612,24 @@ class Engine:
             if worst > 148 * 4:
                 raise InputError(f"local_peer emulation needs tp*batch*4 <= {148 * 4} co-resident all-reduce "
                                  f"CTAs (got {worst})")
+        # all-reduce payload on NVLink: bf16 partials (fp32 sums) halve the bytes in
+        # bf16 mode; fp32 mode keeps fp32 partials (north-star fp32 criterion).
+        # HX_AR_PAYLOAD=fp32|bf16 overrides.
+        payload = os.environ.get("HX_AR_PAYLOAD", "bf16" if self.dtype == torch.bfloat16 else "fp32")
+        if payload == "bf16" and (cfg.hidden_dim % 32 or os.environ.get("HX_AR_MODE", "push") == "pull"):
+            payload = "fp32"
+        self.ar_payload = payload
         if peer_allreduce and self.comm.kind == "dist" and native:
             for e in execs:
                 if e.role.tp > 1:  # fused NVLink all-reduce for the decode step
                     e.par = _ops.PeerAllReduce(e.role.tp_rank, e.role.tp, batch, cfg.hidden_dim, 2 * e.n_layers,
-                                               self.comm.groups[e.role.tp_group], self.comm.dist)
+                                               self.comm.groups[e.role.tp_group], self.comm.dist, payload=payload)
         elif self.local_peer:
             for j in sorted({r.stage for r in roles}):
                 st = sorted((e for e in execs if e.role.stage == j), key=lambda e: e.role.tp_rank)
                 if st[0].role.tp > 1:
                     for e, par in zip(st, _ops.PeerAllReduce.local_group(st[0].role.tp, batch, cfg.hidden_dim,
-                                                                         2 * st[0].n_layers)):
+                                                                         2 * st[0].n_layers, payload=payload)):
                         e.par = par
         for e in execs:
             e.p2p_send, e.p2p_recv, e.ids_send, e.ids_recv = [], None, [], None

@@ -53,6 +53,10 @@ _SIGS = {
     "hx_tp_inbox_init": ([_P, _I, _I, _I, _P], _I),
     "hx_tp_allreduce_push_residual_rmsnorm": ([_P, _P, ctypes.POINTER(ctypes.c_void_p), _I, _I, _I, _P, _P, _P, _I,
                                                _I, _I, _F, _P], _I),
+    "hx_tp_inbox_bytes_ex": ([_I, _I, _I, _I], _SZ),
+    "hx_tp_inbox_init_ex": ([_P, _I, _I, _I, _I, _P], _I),
+    "hx_tp_allreduce_push_residual_rmsnorm_ex": ([_P, _P, ctypes.POINTER(ctypes.c_void_p), _I, _I, _I, _P, _P, _P,
+                                                  _I, _I, _I, _F, _I, _P], _I),
     "hx_handoff_inbox_bytes": ([_SZ], _SZ),
     "hx_handoff_inbox_init": ([_P, _SZ, _P], _I),
     "hx_handoff_push": ([_P, ctypes.POINTER(ctypes.c_void_p), _I, _SZ, _SZ, _P, _P], _I),
@@ -382,8 +386,9 @@ class PeerAllReduce:
     same kernels, each emulated rank launching on its own stream, so the
     protocol runs with real concurrency on a single GPU."""
 
-    def __init__(self, rank: int, tp: int, max_tok: int, hidden: int, sites: int, group, dist, mode: str | None = None):
-        self._setup(rank, tp, max_tok, hidden, sites, mode)
+    def __init__(self, rank: int, tp: int, max_tok: int, hidden: int, sites: int, group, dist, mode: str | None = None,
+                 payload: str = "fp32"):
+        self._setup(rank, tp, max_tok, hidden, sites, mode, payload)
         ptrs = self._alloc_own()
         handles = {}
         lib = load()
@@ -408,12 +413,13 @@ class PeerAllReduce:
         dist.barrier(group=group)
 
     @classmethod
-    def local_group(cls, tp: int, max_tok: int, hidden: int, sites: int, mode: str | None = None):
+    def local_group(cls, tp: int, max_tok: int, hidden: int, sites: int, mode: str | None = None,
+                    payload: str = "fp32"):
         """All ``tp`` ranks of one group in this process (single-GPU emulation)."""
         objs = [cls.__new__(cls) for _ in range(tp)]
         own = []
         for r, o in enumerate(objs):
-            o._setup(r, tp, max_tok, hidden, sites, mode)
+            o._setup(r, tp, max_tok, hidden, sites, mode, payload)
             o._group = o._dist = None
             own.append(o._alloc_own())
         for r, o in enumerate(objs):
@@ -421,10 +427,14 @@ class PeerAllReduce:
         torch.cuda.synchronize()
         return objs
 
-    def _setup(self, rank, tp, max_tok, hidden, sites, mode):
+    def _setup(self, rank, tp, max_tok, hidden, sites, mode, payload="fp32"):
         self.mode = mode or os.environ.get("HX_AR_MODE", "push")
         if self.mode not in ("push", "pull"):
             raise HxError(f"unknown all-reduce mode {self.mode!r}")
+        if payload not in ("fp32", "bf16") or (payload == "bf16" and self.mode != "push"):
+            raise HxError(f"all-reduce payload {payload!r} (mode {self.mode}) not supported")
+        self.payload = payload
+        self._pl = HX_BF16 if payload == "bf16" else HX_F32
         self.rank, self.tp, self.max_tok, self.hidden, self.sites = rank, tp, max_tok, hidden, sites
         self._own, self._opened = [], []
 
@@ -435,13 +445,14 @@ class PeerAllReduce:
         if self.mode == "pull":
             bufs.append(("flags", self.sites * self.max_tok * 8 * 4))
         else:
-            bufs.append(("inbox", int(lib.hx_tp_inbox_bytes(self.tp, self.max_tok, self.hidden))))
+            bufs.append(("inbox", int(lib.hx_tp_inbox_bytes_ex(self.tp, self.max_tok, self.hidden, self._pl))))
         ptrs = {}
         for name, nbytes in bufs:
             ptrs[name] = _alloc(nbytes)
             self._own.append(ptrs[name])
         if self.mode == "push":
-            _check(lib.hx_tp_inbox_init(ptrs["inbox"], self.tp, self.max_tok, self.hidden, None), "hx_tp_inbox_init")
+            _check(lib.hx_tp_inbox_init_ex(ptrs["inbox"], self.tp, self.max_tok, self.hidden, self._pl, None),
+                   "hx_tp_inbox_init_ex")
             torch.cuda.synchronize()
         return ptrs
 
@@ -458,10 +469,10 @@ class PeerAllReduce:
     def allreduce_residual_rmsnorm(self, x, site, gain, out, n_tok, eps):
         lib = load()
         if self.mode == "push":
-            _check(lib.hx_tp_allreduce_push_residual_rmsnorm(
+            _check(lib.hx_tp_allreduce_push_residual_rmsnorm_ex(
                 _p(x), self.peer[f"slot{site % 2}"][self.rank], self._arr["inbox"], self.rank, self.tp, self.max_tok,
                 _p(self.site_state), _p(gain), _p(out), dtype_code(out.dtype) if out is not None else HX_F32,
-                n_tok, self.hidden, eps, _stream()), "hx_tp_allreduce_push_residual_rmsnorm")
+                n_tok, self.hidden, eps, self._pl, _stream()), "hx_tp_allreduce_push_residual_rmsnorm_ex")
             return
         _check(lib.hx_tp_allreduce_residual_rmsnorm(
             _p(x), self._arr[f"slot{site % 2}"], self._arr["flags"], self.rank, self.tp, site, self.max_tok,

@@ -65,6 +65,38 @@ def _run_group(group, xs, parts_per_call, gain, out_dtype, n_tok, eps=1e-5):
 @pytest.mark.parametrize("tp", [2, 4])
 @pytest.mark.parametrize("n_tok,hidden", [(1, 4096), (8, 4096), (32, 8192), (5, 5120)])
 @pytest.mark.parametrize("out_dtype", [torch.bfloat16, torch.float32])
+def test_peer_allreduce_bf16_payload_single_gpu_streams(tp, n_tok, hidden, out_dtype):
+    """bf16 payload: every partial rounded to bf16 once (own included), summed in
+    fp32 in rank order -- residual bitwise x + sum_r float(bf16(p_r)), replicated."""
+    calls, eps = 4, 1e-5
+    g = torch.Generator(device=DEV).manual_seed(tp * 31 + n_tok + hidden)
+    x0 = torch.randn(n_tok, hidden, device=DEV, generator=g)
+    gain = 1 + 0.02 * torch.randn(hidden, device=DEV, generator=g)
+    parts_per_call = []
+    for c in range(calls):
+        parts = [torch.randn(n_tok, hidden, device=DEV, generator=g) for _ in range(tp)]
+        parts[0][0, :9] = -0.0
+        parts[-1][-1, -5:] = -1e-42          # rounds to bf16 -0.0: must not read as the sentinel
+        parts_per_call.append(parts)
+    group = ops.PeerAllReduce.local_group(tp, 32, hidden, 4, mode="push", payload="bf16")
+    xs = [x0.clone() for _ in range(tp)]
+    outs = _run_group(group, xs, parts_per_call, gain, out_dtype, n_tok, eps)
+    for o in group:
+        o.close()
+    x_ref = x0.clone()
+    for c in range(calls):
+        x_ref, y_ref = _ref_allreduce(x_ref, [p.bfloat16().float() for p in parts_per_call[c]], gain, eps)
+        for r in range(tp):
+            tol = 1e-5 if out_dtype == torch.float32 else 8e-3
+            assert (outs[c][r].float() - y_ref).abs().max() <= tol * y_ref.abs().max()
+            assert torch.equal(outs[c][r], outs[c][0])
+    for r in range(tp):
+        assert torch.equal(xs[r], x_ref)
+
+
+@pytest.mark.parametrize("tp", [2, 4])
+@pytest.mark.parametrize("n_tok,hidden", [(1, 4096), (8, 4096), (32, 8192), (5, 5120)])
+@pytest.mark.parametrize("out_dtype", [torch.bfloat16, torch.float32])
 def test_peer_allreduce_single_gpu_streams(tp, n_tok, hidden, out_dtype):
     calls, eps = 5, 1e-5
     g = torch.Generator(device=DEV).manual_seed(tp * 100 + n_tok + hidden)

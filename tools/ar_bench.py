@@ -74,7 +74,34 @@ def main():
         print(f"rank {rank} check push==pull: {same}, replicated: {repl}", flush=True)
         dist.barrier()
         os._exit(0 if same and repl else 1)
-    for mode, n_tok in (("pull", 32), ("push", 8), ("push", 32)):
+    if "--probe-nvls" in sys.argv:   # what torch's symmetric memory offers on this box (NVLS multicast?)
+        try:
+            import torch.distributed._symmetric_memory as symm
+            t = symm.empty(32 * H, device=dev, dtype=torch.float32)
+            hdl = symm.rendezvous(t, dist.group.WORLD.group_name)
+            mc = getattr(hdl, "multicast_ptr", 0)
+            print(f"rank {rank} symm mem: multicast_ptr={mc:#x} has_multicast={bool(mc)}", flush=True)
+            for name in ("one_shot_all_reduce", "two_shot_all_reduce_", "multimem_all_reduce_"):
+                op = getattr(torch.ops.symm_mem, name, None)
+                if op is None:
+                    continue
+                try:
+                    def run(reps, op=op, name=name):
+                        for _ in range(reps):
+                            if name == "one_shot_all_reduce":
+                                op(t, "sum", dist.group.WORLD.group_name)
+                            else:
+                                op(t, "sum", dist.group.WORLD.group_name)
+                    us = timed(run, reps=20, iters=3)
+                    if rank == 0:
+                        print(f"tp={tp} torch symm_mem.{name} 32x{H} fp32: {us:.2f} us/call", flush=True)
+                except Exception as exc:  # noqa: BLE001
+                    if rank == 0:
+                        print(f"symm_mem.{name}: {type(exc).__name__}: {str(exc)[:160]}", flush=True)
+        except Exception as exc:  # noqa: BLE001
+            print(f"rank {rank} symm mem unavailable: {type(exc).__name__}: {str(exc)[:200]}", flush=True)
+    sweep = [("push", n) for n in (1, 8, 16, 32)] if "--sweep" in sys.argv else [("pull", 32), ("push", 8), ("push", 32)]
+    for mode, n_tok in sweep:
         par = ops.PeerAllReduce(rank, tp, n_tok, H, 80, dist.group.WORLD, dist, mode=mode)
         x = torch.randn(n_tok, H, device=dev)
         gain = torch.ones(H, device=dev)
