@@ -163,8 +163,8 @@ int hx_tp_allreduce_residual_rmsnorm(float *x, const float *const *parts, int *c
  * for the peers' rows (sentinel -0.0f until the data lands). inboxes[r] = rank
  * r's inbox of hx_tp_inbox_bytes(tp, max_tok, hidden) bytes (peer-mapped; own
  * local), armed once with hx_tp_inbox_init; own_part = this rank's partial
- * [n_tok][hidden]; state = this rank's int[2] call counter (zeroed). Same
- * result bits as hx_tp_allreduce_residual_rmsnorm. */
+ * [n_tok][hidden]; state = this rank's per-CTA call counters, int[4 * max_tok]
+ * (zeroed once). Same result bits as hx_tp_allreduce_residual_rmsnorm. */
 size_t hx_tp_inbox_bytes(int tp, int max_tok, int hidden);
 int hx_tp_inbox_init(void *inbox, int tp, int max_tok, int hidden, hx_stream_t stream);
 int hx_tp_allreduce_push_residual_rmsnorm(float *x, const float *own_part, float *const *inboxes,

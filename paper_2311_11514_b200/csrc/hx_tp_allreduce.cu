@@ -127,8 +127,10 @@ __global__ void __launch_bounds__(1024)
 // rank's call k + 1 data, pushed after this kernel has completed).
 // One token row = a cluster of AR_CL CTAs, each owning hidden / AR_CL features,
 // so the push/poll traffic spreads over 4x the SMs; the RMS sum of squares is
-// combined across the cluster through DSMEM. The call counter lives in
-// state[0] and is bumped by the grid's last CTA.
+// combined across the cluster through DSMEM. Call counters are per CTA:
+// state[c] counts the calls CTA c (= token row t, feature slice c % AR_CL)
+// took part in -- every inbox location is always served by the same CTA index
+// on every rank, so no cross-CTA atomics sit on the kernel's completion path.
 struct ArInbox {
   float *box[kMaxTP];  // rank r's inbox (peer-mapped; own = local)
 };
@@ -207,7 +209,7 @@ __global__ void __launch_bounds__(256)
   if (out && threadIdx.x < per / 32)   // the gain is a weight: pull this CTA's slice into L1 before the wait
     asm volatile("prefetch.global.L1 [%0];" ::"l"(gain + base + threadIdx.x * 32));
   pdl_wait();  // this rank's partial (previous kernel) is complete
-  const int call = *(volatile int *)state;
+  const int call = *(volatile int *)(state + blockIdx.x);
   const int buf = call & 1;
   // inbox element index of (buffer, sender r, token t, feature n); payload elements of PL
   constexpr int V = ArPayload<PL>::V;   // features per 16-byte vector
@@ -297,14 +299,8 @@ __global__ void __launch_bounds__(256)
       }
     }
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const int done = atomicAdd(state + 1, 1);
-    if (done == (int)gridDim.x - 1) {
-      state[1] = 0;
-      *(volatile int *)state = call + 1;
-    }
-  }
+  __syncthreads();  // every thread has read `call`
+  if (threadIdx.x == 0) *(volatile int *)(state + blockIdx.x) = call + 1;
 }
 
 __global__ void fill_u32_kernel(uint32_t *p, size_t n, uint32_t v) {

@@ -458,7 +458,8 @@ class PeerAllReduce:
 
     def _finish(self, peer: dict):
         self.peer = peer
-        self.site_state = torch.zeros(2 * self.sites, dtype=torch.int32, device="cuda")
+        # pull mode: [epoch, done] per call site; push mode: one call counter per CTA (4 per token row)
+        self.site_state = torch.zeros(max(2 * self.sites, 4 * self.max_tok), dtype=torch.int32, device="cuda")
         self._arr = {name: (ctypes.c_void_p * self.tp)(*peer[name]) for name in peer}
 
     def slot(self, site: int) -> torch.Tensor:

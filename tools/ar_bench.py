@@ -100,9 +100,11 @@ def main():
                         print(f"symm_mem.{name}: {type(exc).__name__}: {str(exc)[:160]}", flush=True)
         except Exception as exc:  # noqa: BLE001
             print(f"rank {rank} symm mem unavailable: {type(exc).__name__}: {str(exc)[:200]}", flush=True)
-    sweep = [("push", n) for n in (1, 8, 16, 32)] if "--sweep" in sys.argv else [("pull", 32), ("push", 8), ("push", 32)]
+    sweep = ([(m, n) for m in ("push", "push-bf16") for n in (1, 8, 16, 32)] if "--sweep" in sys.argv
+             else [("pull", 32), ("push", 8), ("push", 32), ("push-bf16", 32)])
     for mode, n_tok in sweep:
-        par = ops.PeerAllReduce(rank, tp, n_tok, H, 80, dist.group.WORLD, dist, mode=mode)
+        par = ops.PeerAllReduce(rank, tp, n_tok, H, 80, dist.group.WORLD, dist, mode=mode.split("-")[0],
+                                payload="bf16" if mode.endswith("bf16") else "fp32")
         x = torch.randn(n_tok, H, device=dev)
         gain = torch.ones(H, device=dev)
         out = torch.empty(n_tok, H, device=dev, dtype=torch.bfloat16)
