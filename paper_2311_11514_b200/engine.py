@@ -609,9 +609,9 @@ class Engine:
         self.local_peer = bool(local_peer and self.comm.kind == "local" and native and peer_allreduce)
         if self.local_peer:
             worst = max(r.tp for r in roles) * batch * 4
-            if worst > 148 * 4:
-                raise InputError(f"local_peer emulation needs tp*batch*4 <= {148 * 4} co-resident all-reduce "
-                                 f"CTAs (got {worst})")
+            if worst > _ops.PEER_AR_CORESIDENT:
+                raise InputError(f"local_peer emulation needs tp*batch*4 <= {_ops.PEER_AR_CORESIDENT} co-resident "
+                                 f"all-reduce CTAs (got {worst})")
         # all-reduce payload on NVLink: bf16 partials (fp32 sums) halve the bytes in
         # bf16 mode; fp32 mode keeps fp32 partials (north-star fp32 criterion).
         # HX_AR_PAYLOAD=fp32|bf16 overrides.

@@ -369,6 +369,12 @@ def _alloc(nbytes: int) -> int:
     return p.value
 
 
+#: CTAs of the push all-reduce that fit on one B200 at once (4 per token row,
+#: __launch_bounds__(256, 2): 2 per SM x 148 SMs). A single-GPU emulation runs
+#: every rank's kernel concurrently, so tp * n_tok * 4 must not exceed it.
+PEER_AR_CORESIDENT = 2 * 148
+
+
 class PeerAllReduce:
     """Per-rank state of the fused NVLink all-reduce + residual + RMSNorm of a
     TP>1 decode step. Buffers are cudaIpc-exportable allocations mapped on every

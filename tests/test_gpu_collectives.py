@@ -68,6 +68,7 @@ def _run_group(group, xs, parts_per_call, gain, out_dtype, n_tok, eps=1e-5):
 def test_peer_allreduce_bf16_payload_single_gpu_streams(tp, n_tok, hidden, out_dtype):
     """bf16 payload: every partial rounded to bf16 once (own included), summed in
     fp32 in rank order -- residual bitwise x + sum_r float(bf16(p_r)), replicated."""
+    n_tok = min(n_tok, ops.PEER_AR_CORESIDENT // (4 * tp))   # all emulated ranks' CTAs co-resident
     calls, eps = 4, 1e-5
     g = torch.Generator(device=DEV).manual_seed(tp * 31 + n_tok + hidden)
     x0 = torch.randn(n_tok, hidden, device=DEV, generator=g)
@@ -98,6 +99,7 @@ def test_peer_allreduce_bf16_payload_single_gpu_streams(tp, n_tok, hidden, out_d
 @pytest.mark.parametrize("n_tok,hidden", [(1, 4096), (8, 4096), (32, 8192), (5, 5120)])
 @pytest.mark.parametrize("out_dtype", [torch.bfloat16, torch.float32])
 def test_peer_allreduce_single_gpu_streams(tp, n_tok, hidden, out_dtype):
+    n_tok = min(n_tok, ops.PEER_AR_CORESIDENT // (4 * tp))   # all emulated ranks' CTAs co-resident
     calls, eps = 5, 1e-5
     g = torch.Generator(device=DEV).manual_seed(tp * 100 + n_tok + hidden)
     x0 = torch.randn(n_tok, hidden, device=DEV, generator=g)
