@@ -199,6 +199,15 @@ int hx_handoff_push(const void *src, void *const *dst_inboxes, int n_dst, size_t
                     size_t max_words, int *state, hx_stream_t stream);
 int hx_handoff_pull(void *dst, void *inbox, size_t words, size_t max_words, int *state,
                     hx_stream_t stream);
+/* Flow-controlled variant for streams of hand-offs the sender may run ahead on
+ * (the pipelined prefill's micro-batches): the receiver drains hand-off k from
+ * buffer k % 3, re-arms it in place and publishes credit k + 1 in the inbox's
+ * credit word; the sender's hand-off k waits (over NVLink) for credit >= k - 2
+ * before storing. One destination per call; state as above (int[2], zeroed),
+ * separate from the decode links'. */
+int hx_handoff_push_credit(const void *src, void *dst_inbox, size_t words, size_t max_words, int *state,
+                           hx_stream_t stream);
+int hx_handoff_pull_credit(void *dst, void *inbox, size_t words, size_t max_words, int *state, hx_stream_t stream);
 
 /* ---- Prefill attention on tcgen05 (whole prompt, no earlier context).
  * hx_prefill_vt writes the prompt's V transposed per (sequence, kv head):

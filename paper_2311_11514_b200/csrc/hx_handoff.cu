@@ -114,6 +114,97 @@ __global__ void __launch_bounds__(256)
   bump_call(state, call);
 }
 
+// ------------------------------------------------------------- credit-based stream (prefill)
+// The prefill's stage j pushes micro-batch after micro-batch without waiting for
+// stage j+1, so the decode protocol's "the sender cannot lap the receiver"
+// argument does not hold. Flow control by credits: the inbox carries a credit
+// word after its 3 buffers (kCreditOffset); the receiver, after copying
+// hand-off k out of buffer k % 3 and re-arming that buffer in place, publishes
+// credit = k + 1 (release, system scope); the sender's hand-off k first waits
+// (acquire, over NVLink) until credit >= k - 2, i.e. buffer k % 3 was drained.
+__device__ __forceinline__ int ld_acquire_sys_s32(const int *p) {
+  int v;
+  asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys_s32(int *p, int v) {
+  asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__host__ __device__ __forceinline__ int *credit_word(uint32_t *inbox, size_t max_words) {
+  return reinterpret_cast<int *>(inbox + 3 * max_words);
+}
+
+__global__ void __launch_bounds__(256)
+    handoff_push_credit_kernel(const uint32_t *__restrict__ src, uint32_t *box, size_t words, size_t max_words,
+                               int *state) {
+  pdl_trigger();
+  pdl_wait();  // src was written by the previous kernel
+  const int call = *(volatile int *)state;
+  if (threadIdx.x == 0) {
+    const int *credit = credit_word(box, max_words);
+    for (uint32_t spins = 0; ld_acquire_sys_s32(credit) < call - 2; ++spins)
+      if (spins > (1u << 26)) __trap();  // the receiver never drained: fail loudly, never hang
+  }
+  __syncthreads();
+  uint32_t *dst = box + (size_t)(call % 3) * max_words;
+  const size_t nv = words / 4;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nv; i += stride) {
+    uint4 v = __ldcs(reinterpret_cast<const uint4 *>(src) + i);
+    v.x = hand_clean(v.x); v.y = hand_clean(v.y); v.z = hand_clean(v.z); v.w = hand_clean(v.w);
+    reinterpret_cast<uint4 *>(dst)[i] = v;
+  }
+  for (size_t i = nv * 4 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < words; i += stride)
+    dst[i] = hand_clean(src[i]);
+  bump_call(state, call);
+}
+
+__global__ void __launch_bounds__(256)
+    handoff_pull_credit_kernel(uint32_t *__restrict__ dst, uint32_t *inbox, size_t words, size_t max_words,
+                               int *state) {
+  pdl_trigger();
+  pdl_wait();  // the previous kernel may still read dst
+  const int call = *(volatile int *)state;
+  uint32_t *buf = inbox + (size_t)(call % 3) * max_words;
+  const size_t nv = words / 4;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const uint4 s4 = make_uint4(kHandoffSentinel, kHandoffSentinel, kHandoffSentinel, kHandoffSentinel);
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nv; i += stride) {
+    uint4 *p = reinterpret_cast<uint4 *>(buf) + i;
+    uint4 v = ld_volatile_v4(p);
+    for (uint32_t spins = 0; v.x == kHandoffSentinel || v.y == kHandoffSentinel || v.z == kHandoffSentinel ||
+                             v.w == kHandoffSentinel;
+         ++spins) {
+      if (spins > (1u << 26)) __trap();
+      v = ld_volatile_v4(p);
+    }
+    reinterpret_cast<uint4 *>(dst)[i] = v;
+    *p = s4;  // drained: re-arm in place
+  }
+  for (size_t i = nv * 4 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < words; i += stride) {
+    uint32_t v = ld_volatile_u32(buf + i);
+    for (uint32_t spins = 0; v == kHandoffSentinel; ++spins) {
+      if (spins > (1u << 26)) __trap();
+      v = ld_volatile_u32(buf + i);
+    }
+    dst[i] = v;
+    buf[i] = kHandoffSentinel;
+  }
+  // every CTA's re-arm stores are visible before the last CTA hands the buffer back
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    const int done = atomicAdd(state + 1, 1);
+    if (done == (int)gridDim.x - 1) {
+      state[1] = 0;
+      *(volatile int *)state = call + 1;
+      __threadfence_system();
+      st_release_sys_s32(credit_word(inbox, max_words), call + 1);
+    }
+  }
+}
+
 __global__ void handoff_fill_kernel(uint32_t *p, size_t n) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     p[i] = kHandoffSentinel;
@@ -129,10 +220,12 @@ static int handoff_grid(size_t words) {
 
 using namespace hx;
 
-extern "C" size_t hx_handoff_inbox_bytes(size_t max_words) { return 3 * max_words * sizeof(uint32_t); }
+// 3 buffers of max_words words, then the credit word of the flow-controlled (prefill) protocol
+extern "C" size_t hx_handoff_inbox_bytes(size_t max_words) { return 3 * max_words * sizeof(uint32_t) + 128; }
 
 extern "C" int hx_handoff_inbox_init(void *inbox, size_t max_words, hx_stream_t stream) {
   if (!inbox || !max_words || max_words % 4) return HX_ERR_ARG;
+  cudaMemsetAsync(credit_word((uint32_t *)inbox, max_words), 0, 128, as_stream(stream));
   // Load both ends of the protocol now: under CUDA lazy loading the first launch
   // of a kernel loads its module, which cannot complete while a spinning pull
   // occupies the device -- a pull launched before the push's first-ever launch in
@@ -140,6 +233,8 @@ extern "C" int hx_handoff_inbox_init(void *inbox, size_t max_words, hx_stream_t 
   cudaFuncAttributes fa;
   cudaFuncGetAttributes(&fa, handoff_push_kernel);
   cudaFuncGetAttributes(&fa, handoff_pull_kernel);
+  cudaFuncGetAttributes(&fa, handoff_push_credit_kernel);
+  cudaFuncGetAttributes(&fa, handoff_pull_credit_kernel);
   handoff_fill_kernel<<<148, 256, 0, as_stream(stream)>>>((uint32_t *)inbox, 3 * max_words);
   return launch_status();
 }
@@ -161,5 +256,21 @@ extern "C" int hx_handoff_pull(void *dst, void *inbox, size_t words, size_t max_
   if (!dst || !inbox || !state || max_words % 4 || words > max_words || (uintptr_t)dst % 16) return HX_ERR_ARG;
   if (words == 0) return 0;
   return launch(handoff_pull_kernel, dim3(handoff_grid(max_words)), dim3(256), 0, as_stream(stream),
+                (uint32_t *)dst, (uint32_t *)inbox, words, max_words, state);
+}
+
+extern "C" int hx_handoff_push_credit(const void *src, void *dst_inbox, size_t words, size_t max_words, int *state,
+                                      hx_stream_t stream) {
+  if (!src || !dst_inbox || !state || max_words % 4 || words > max_words || (uintptr_t)src % 16) return HX_ERR_ARG;
+  if (words == 0) return 0;
+  return launch(handoff_push_credit_kernel, dim3(handoff_grid(words)), dim3(256), 0, as_stream(stream),
+                (const uint32_t *)src, (uint32_t *)dst_inbox, words, max_words, state);
+}
+
+extern "C" int hx_handoff_pull_credit(void *dst, void *inbox, size_t words, size_t max_words, int *state,
+                                      hx_stream_t stream) {
+  if (!dst || !inbox || !state || max_words % 4 || words > max_words || (uintptr_t)dst % 16) return HX_ERR_ARG;
+  if (words == 0) return 0;
+  return launch(handoff_pull_credit_kernel, dim3(handoff_grid(words)), dim3(256), 0, as_stream(stream),
                 (uint32_t *)dst, (uint32_t *)inbox, words, max_words, state);
 }

@@ -211,6 +211,7 @@ class RankExecutor:
         self.vr = cfg.vocab // tp
         self.qkv_n = (self.hq + 2 * self.hkv) * self.hd
         self.batch, self.max_prompt, self.max_out = batch, max_prompt, max_out
+        self.cur_b = batch        # sequences of the request in flight (<= batch)
         self.max_ctx = max_prompt + max_out
         self.n_layers = role.layers[1] - role.layers[0]
         H = cfg.hidden_dim
@@ -376,7 +377,7 @@ class RankExecutor:
 
     def head(self, prefill_len: int):
         """final norm on each sequence's last row + vocab-parallel lm_head + local argmax."""
-        k, H, b = self.k, self.cfg.hidden_dim, self.batch
+        k, H, b = self.k, self.cfg.hidden_dim, self.cur_b
         if prefill_len:
             xs = self.x.view(-1)[(prefill_len - 1) * H:]
             k.rmsnorm(xs, self.w["norm"], self.hl, b, self.cfg.rms_eps, ldx=prefill_len * H)
@@ -386,7 +387,7 @@ class RankExecutor:
         k.argmax_partial(self.logits, self.keys, b, self.vr, self.role.tp_rank * self.vr)
 
     def finalize(self):
-        self.k.argmax_finalize(self.keys, self.ids, self.history, self.step, self.batch, bump=True)
+        self.k.argmax_finalize(self.keys, self.ids, self.history, self.step, self.cur_b, bump=True)
 
 
 # --------------------------------------------------------------------- driver
@@ -519,6 +520,10 @@ class StageDriver:
                 for link in e.p2p_send:
                     link.push(e.x[:n_tok])
                 return
+            if not decode and e.pf_send:   # prefill micro-batch: flow-controlled NVLink P2P
+                for link in e.pf_send:
+                    link.push_credit(e.x[:n_tok])
+                return
             for dst in e.role.send_to:
                 self.comm.send(e.x[:n_tok], e.role.device, dst)
         self._each(one)
@@ -527,6 +532,9 @@ class StageDriver:
         def one(e):
             if decode and e.p2p_recv is not None:
                 e.p2p_recv.pull(e.x[:n_tok])
+                return
+            if not decode and e.pf_recv is not None:
+                e.pf_recv.pull_credit(e.x[:n_tok])
                 return
             self.comm.recv(e.x[:n_tok], e.role.recv_from, e.role.device)
         self._each(one)
@@ -633,6 +641,7 @@ class Engine:
                         e.par = par
         for e in execs:
             e.p2p_send, e.p2p_recv, e.ids_send, e.ids_recv = [], None, [], None
+            e.pf_send, e.pf_recv = [], None
         self._p2p = ((self.comm.kind == "dist" or self.local_peer) and native
                      and self.num_stages > 1 and os.environ.get("HX_P2P", "1") != "0")
         if self._p2p:
@@ -645,6 +654,7 @@ class Engine:
         self.use_graphs = use_graphs and self.device.type == "cuda"
         self._graphs = None
         self._graph_key = None
+        self._graph_cache = {}
         self._graph_launches = []
         self._replayed = 0
 
@@ -656,9 +666,16 @@ class Engine:
         for r in self.roles:
             links += [("hidden", r.device, dst) for dst in r.send_to]
             links += [("ids", r.device, dst) for dst in r.ids_send_to]
+        # the pipelined prefill's hand-offs use their own flow-controlled links
+        # (hx_handoff_push/pull_credit), sized for one prefill micro-batch
+        if os.environ.get("HX_P2P_PREFILL", "1") != "0":
+            links += [("prefill", src, dst) for kind, src, dst in list(links) if kind == "hidden"]
+        mb_rows = (self.batch // self.prefill_microbatches(self.batch, self.max_prompt)) * self.max_prompt
+        self._pf_rows_cap = mb_rows
         mine = {e.role.device: e for e in execs}
         for kind, src, dst in sorted(links):
-            words = self.batch * (self.cfg.hidden_dim if kind == "hidden" else 1)
+            words = {"hidden": self.batch * self.cfg.hidden_dim, "ids": self.batch,
+                     "prefill": mb_rows * self.cfg.hidden_dim}[kind]
             if self.local_peer:           # both ends in this process
                 link = _ops.P2PLink.local(src, dst, words)
                 ends = [(mine[src], True), (mine[dst], False)]
@@ -670,7 +687,12 @@ class Engine:
                                     self.comm.dist)
                 ends = [(mine[me], me == src)]
             for e, sender in ends:
-                if kind == "hidden":
+                if kind == "prefill":
+                    if sender:
+                        e.pf_send.append(link)
+                    else:
+                        e.pf_recv = link
+                elif kind == "hidden":
                     if sender:
                         e.p2p_send.append(link)
                     else:
@@ -697,6 +719,9 @@ class Engine:
         for m in range(1, 17):   # 70B [2,1,1] b=32 x 1024: m=4 1.75 s, 8 1.51 s, 16 1.45 s
             if b % m == 0 and (b // m) * s >= 2048:
                 best = m
+        cap = getattr(self, "_pf_rows_cap", None)   # a micro-batch must fit the prefill P2P inbox
+        while cap is not None and (b // best) * s > cap:
+            best = next(m for m in range(best + 1, b + 1) if b % m == 0)
         return best
 
     def _prefill(self, b, s):
@@ -799,7 +824,9 @@ class Engine:
         """One CUDA graph per local stage for the decode compute (collectives
         inside; stage hand-offs stay outside on the same stream)."""
         key = b
-        if self._graphs is not None and self._graph_key == key:
+        if key in self._graph_cache:   # one set of graphs per batch size served
+            self._graphs, self._graph_launches = self._graph_cache[key]
+            self._graph_key = key
             return self._graphs
         graphs, counts = [], []
         if self.local_peer:   # one graph over every emulated rank's stream (fork / join by events)
@@ -808,6 +835,7 @@ class Engine:
             with torch.cuda.graph(g, capture_error_mode="thread_local"):
                 self._decode_emulated_peer(b)
             self._graphs, self._graph_key, self._graph_launches = [g], key, [self._launch_count() - n0]
+            self._graph_cache[key] = (self._graphs, self._graph_launches)
             return self._graphs
         for d in self.drivers:
             g = torch.cuda.CUDAGraph()
@@ -821,6 +849,7 @@ class Engine:
             counts.append(self._launch_count() - n0)
             graphs.append(g)
         self._graphs, self._graph_key, self._graph_launches = graphs, key, counts
+        self._graph_cache[key] = (graphs, counts)
         return graphs
 
     def _launch_count(self) -> int:
@@ -851,12 +880,12 @@ class Engine:
         if b > self.batch or s > self.max_prompt or s_out > self.max_out:
             raise InputError(f"request {(b, s, s_out)} exceeds engine shape "
                              f"{(self.batch, self.max_prompt, self.max_out)}")
-        if b != self.batch:
-            raise InputError("static batching: batch must equal the engine batch")
+        for e in self.execs:        # any batch up to the engine's: kernels run on the first b rows
+            e.cur_b = b
         cuda = self.device.type == "cuda"
         if cuda and self.use_graphs and not return_logits:
-            # warm the eager path once (kernel attributes, NCCL comms) before capture
-            if self._graphs is None:
+            # warm the eager path once per batch size (kernel attributes, NCCL comms) before capture
+            if b not in self._graph_cache:
                 self._reset(b, s, s_out)
                 for e in self.execs:
                     if e.role.is_first:
@@ -865,7 +894,7 @@ class Engine:
                 self._decode_step(b, None)
                 torch.cuda.synchronize(self.device)
                 self._capture(b)
-        graphs = self._graphs if (cuda and self.use_graphs and not return_logits) else None
+        graphs = self._capture(b) if (cuda and self.use_graphs and not return_logits) else None
         self._replayed = 0
         n_launch0 = self._launch_count()
         self._reset(b, s, s_out)
@@ -924,7 +953,7 @@ class Engine:
 
     def _force(self, forced_dev, t):
         for e in self._last_execs():
-            e.ids.copy_(forced_dev[:, t])
+            e.ids[:forced_dev.shape[0]].copy_(forced_dev[:, t])
 
     def _last_execs(self):
         return [e for e in self.execs if e.role.is_last]
@@ -946,15 +975,17 @@ class Engine:
         """Release the NVLink peer state (unmap peers' IPC buffers, free own
         ones, after a group barrier) and the captured graphs. Idempotent."""
         self._graphs = None
+        self._graph_cache = {}
         links = {}
         for e in self.execs:
             if e.par is not None:
                 e.par.close()
                 e.par = None
-            for link in list(e.p2p_send) + list(e.ids_send) + [e.p2p_recv, e.ids_recv]:
+            for link in list(e.p2p_send) + list(e.ids_send) + list(e.pf_send) + [e.p2p_recv, e.ids_recv, e.pf_recv]:
                 if link is not None:
                     links[id(link)] = link      # an emulated link is held by both of its ends
             e.p2p_send, e.ids_send, e.p2p_recv, e.ids_recv = [], [], None, None
+            e.pf_send, e.pf_recv = [], None
         for link in links.values():
             link.close()
 

@@ -61,6 +61,8 @@ _SIGS = {
     "hx_handoff_inbox_init": ([_P, _SZ, _P], _I),
     "hx_handoff_push": ([_P, ctypes.POINTER(ctypes.c_void_p), _I, _SZ, _SZ, _P, _P], _I),
     "hx_handoff_pull": ([_P, _P, _SZ, _SZ, _P, _P], _I),
+    "hx_handoff_push_credit": ([_P, _P, _SZ, _SZ, _P, _P], _I),
+    "hx_handoff_pull_credit": ([_P, _P, _SZ, _SZ, _P, _P], _I),
     "hx_prefill_vt": ([_P, _P, _I, _I, _I, _I, _I, _P], _I),
     "hx_attn_prefill_tc": ([_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P], _I),
     "hx_splitk_swiglu": ([_P, _I, _P, _I, _I, _I, _P, _I, _P], _I),
@@ -564,6 +566,18 @@ class P2PLink:
         """Receiver: wait for this hand-off's data and copy it into ``t``."""
         _check(load().hx_handoff_pull(_p(t), self._own, t.numel() * t.element_size() // 4, self.max_words,
                                       _p(self.recv_state), _stream()), "hx_handoff_pull")
+
+    def push_credit(self, t: torch.Tensor):
+        """Sender, flow-controlled stream (prefill micro-batches): wait until the
+        target buffer was drained, then store ``t`` into it."""
+        _check(load().hx_handoff_push_credit(_p(t), self._peer, t.numel() * t.element_size() // 4, self.max_words,
+                                             _p(self.state), _stream()), "hx_handoff_push_credit")
+
+    def pull_credit(self, t: torch.Tensor):
+        """Receiver, flow-controlled stream: copy the next hand-off into ``t``,
+        re-arm its buffer and hand the buffer back to the sender."""
+        _check(load().hx_handoff_pull_credit(_p(t), self._own, t.numel() * t.element_size() // 4, self.max_words,
+                                             _p(self.recv_state), _stream()), "hx_handoff_pull_credit")
 
     def close(self):
         lib = load()

@@ -29,7 +29,9 @@ def test_request_shape_checks():
     with pytest.raises(InputError):
         eng.generate(np.zeros((2, 9), np.int32), 4)
     with pytest.raises(InputError):
-        eng.generate(np.zeros((1, 8), np.int32), 4)
+        eng.generate(np.zeros((3, 8), np.int32), 4)     # more sequences than the engine holds
+    with pytest.raises(InputError):
+        eng.generate(np.zeros((2, 8), np.int32), 5)     # more outputs than the KV cache holds
     t = eng.service_time(TaskSpec(2, 8, 3))
     assert t > 0
 
@@ -72,3 +74,14 @@ def test_microbatched_prefill_matches_golden(tps, layers, monkeypatch):
     r = eng.generate(G["prompt"], 16, return_logits=True)
     assert np.array_equal(r.ids, G["ids"])
     assert np.abs(r.logits[..., G["cols"]] - G["col_val"]).max() / G["max_abs"] < 1e-3
+
+
+def test_smaller_batch_than_engine_matches_golden():
+    """Requests of any batch up to the engine's: b=1 and b=2 on a b=3 engine give
+    the golden ids of their sequences (the kernels run on the first b rows)."""
+    eng = Engine(simple_plan([2, 1], [3, 1]), TINY, dtype="fp32", batch=3, max_prompt=64, max_out=16,
+                 device="cpu", kernels=cpu_kernels, page_size=16)
+    r2 = eng.generate(G["prompt"], 16)
+    assert np.array_equal(r2.ids, G["ids"])
+    r1 = eng.generate(G["prompt"][1:2], 16)
+    assert np.array_equal(r1.ids, G["ids"][1:2])

@@ -264,3 +264,30 @@ def test_handoff_push_multi_destination():
         assert torch.equal(da, src) and torch.equal(db, src)
     a.close()
     b.close()
+
+
+@pytest.mark.parametrize("words", [4096 * 64, 1000 * 8 + 3])
+def test_credit_handoff_sender_runs_ahead(words):
+    """The prefill stream of hand-offs (hx_handoff_push/pull_credit): the sender
+    queues 7 micro-batches before the receiver drains any -- its 4th push must
+    wait (over the credit word) until buffer 0 was drained, re-armed and handed
+    back; every micro-batch arrives intact and in order."""
+    link = ops.P2PLink.local(0, 1, words)
+    g = torch.Generator(device=DEV).manual_seed(words % 97)
+    n = 7
+    srcs = [torch.randn(words - 4 * (k % 2), device=DEV, generator=g) for k in range(n)]
+    for s_ in srcs:
+        s_[:2] = -0.0
+    dsts = [torch.full_like(s_, float("nan")) for s_ in srcs]
+    torch.cuda.synchronize()
+    send, recv = torch.cuda.Stream(), torch.cuda.Stream()
+    with torch.cuda.stream(send):
+        for s_ in srcs:
+            link.push_credit(s_)
+    with torch.cuda.stream(recv):
+        for d in dsts:
+            link.pull_credit(d)
+    torch.cuda.synchronize()
+    for s_, d in zip(srcs, dsts):
+        assert torch.equal(d, s_ + 0.0)
+    link.close()

@@ -182,3 +182,15 @@ def test_kernel_launches_are_counted():
     n0 = ops.launch_count()
     eng.generate(G["prompt"], 4)
     assert ops.launch_count() - n0 > 4 * 10
+
+
+def test_smaller_batch_requests_share_one_engine():
+    """One engine serves requests of different batch sizes (<= its batch), each
+    with its own captured decode graph; ids equal the golden ones per sequence.
+    Runs the emulated [2,1] plan through the multi-GPU collective kernels."""
+    eng = Engine(simple_plan([2, 1], [3, 1]), TINY, dtype="fp32", batch=2, max_prompt=64, max_out=16,
+                 device="cuda:0", page_size=16, local_peer=True)
+    for rows in ([1], [0, 1], [0], [0, 1]):
+        r = eng.generate(G["prompt"][rows], 16)
+        assert np.array_equal(r.ids, G["ids"][rows]), rows
+    assert set(eng._graph_cache) == {1, 2}
