@@ -1174,31 +1174,11 @@ static int linear_impl(const void *w, const void *x, void *y, int dtype, int y_d
         default: return launch_sk<64, 4, true>(ma, mb, sk, st);
       }
     }
+    // ring depths 6 / 5 / 4 (BN 16 / 32 / 64): deeper rings (HX_SK_STAGES 8-12,
+    // HX_SK32_STAGES 7-9 in round 1) measured neutral and were dropped
     switch (pl.bn) {
-      case 16: {
-        static const int stages = [] {
-          const char *e = getenv("HX_SK_STAGES");
-          return e ? atoi(e) : 6;
-        }();
-        switch (stages) {
-          case 4: return launch_sk<16, 4>(ma, mb, sk, st);
-          case 8: return launch_sk<16, 8>(ma, mb, sk, st);
-          case 10: return launch_sk<16, 10>(ma, mb, sk, st);
-          case 12: return launch_sk<16, 12>(ma, mb, sk, st);
-          default: return launch_sk<16, 6>(ma, mb, sk, st);
-        }
-      }
-      case 32: {
-        static const int stages = [] {
-          const char *e = getenv("HX_SK32_STAGES");
-          return e ? atoi(e) : 5;
-        }();
-        switch (stages) {
-          case 7: return launch_sk<32, 7>(ma, mb, sk, st);
-          case 9: return launch_sk<32, 9>(ma, mb, sk, st);
-          default: return launch_sk<32, 5>(ma, mb, sk, st);
-        }
-      }
+      case 16: return launch_sk<16, 6>(ma, mb, sk, st);
+      case 32: return launch_sk<32, 5>(ma, mb, sk, st);
       default: return launch_sk<64, 4>(ma, mb, sk, st);
     }
   } else {
