@@ -1,6 +1,9 @@
-"""Small invocations of every hx kernel family for compute-sanitizer
-(memcheck / racecheck / synccheck), one process, everything on one stream.
+"""Small invocations of every hx kernel family, one process, everything on one
+stream -- a quick all-kernels check, and the input for compute-sanitizer
+(memcheck / racecheck / synccheck) where it is available (it is closed on the
+gpurun pool this repo was measured on):
 
+    python tools/sanitize.py
     compute-sanitizer --tool memcheck python tools/sanitize.py
 
 The multi-rank spin protocols (push all-reduce, concurrent hand-offs) need
