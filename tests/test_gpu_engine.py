@@ -121,6 +121,15 @@ def test_llama70b_widths_emulated_42_peer_kernels():
     _bf16_check(cfg, [4, 2], [1, 1], 4, 64, 6, local_peer=True)
 
 
+def test_llama70b_widths_c4_topology_emulated_peer_kernels():
+    """The C4 plan's topology, [4,2,2], at Llama-2-70B widths (one layer per
+    stage), all 8 ranks on one GPU through the multi-GPU kernels: TP=4 and TP=2
+    all-reduces, the 4 -> 2 and 2 -> 2 decode hand-offs, the 2 -> 4 token
+    return and the prefill's credit hand-offs."""
+    cfg = preset("llama2-70b", num_layers=3)
+    _bf16_check(cfg, [4, 2, 2], [1, 1, 1], 4, 64, 5, local_peer=True)
+
+
 def test_llama7b_full_depth_c2():
     """C2 exactly: Llama-2-7B, all 32 layers, b=8, s_in=512, host-seeded
     weights, 4 teacher-forced steps (forced ids: seeded random tokens) against
