@@ -342,6 +342,156 @@ __global__ void __launch_bounds__(128, 1)
   if (warp == 1) tmem_dealloc(tmem, TMEM_COLS);
 }
 
+// ------------------------------------------------------------------ persistent prefill GEMM
+// Prefill (token-major) Y = X W^T on whole 128 x BN tiles, persistent: one CTA
+// per SM walks the tiles blockIdx.x, blockIdx.x + G, ... in the grouped
+// raster order of gemm_bf16_tc_kernel. Warp 0 streams the A (activation) and B
+// (packed weight) K-blocks of all its tiles through one mbarrier ring without
+// a per-tile refill; warp 1 issues the MMAs of tile k into TMEM buffer k & 1
+// while warps 2-5 drain tile k - 1 from the other buffer (2 x BN = 512 TMEM
+// columns), so the epilogue and the next tile's pipeline fill hide behind the
+// tensor core instead of running between CTAs.
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(192, 1)
+    gemm_tc_persistent_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
+                              const __grid_constant__ GemmArgs p) {
+  constexpr uint32_t A_BYTES = BM * BK * 2;
+  constexpr uint32_t B_BYTES = BN * BK * 2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *sa = smem;
+  uint8_t *sb = smem + STAGES * A_BYTES;
+  uint64_t *full = reinterpret_cast<uint64_t *>(sb + STAGES * B_BYTES);
+  uint64_t *empty = full + STAGES;
+  uint64_t *tfull = empty + STAGES;   // [2]
+  uint64_t *tempty = tfull + 2;       // [2]
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+  pdl_trigger();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int GM = 16;
+  const int Mt = (p.M + BM - 1) / BM, Nt = (p.N + BN - 1) / BN;
+  const int tiles = Mt * Nt, G = gridDim.x;
+  const int nkb = p.kb_total;
+  auto tile_mn = [&](int pid, int &tm, int &tn) {  // grouped rasterisation (L2 reuse of X rows / W columns)
+    const int first_m = (pid / (GM * Nt)) * GM;
+    const int gm = min(Mt - first_m, GM);
+    tm = first_m + (pid % (GM * Nt)) % gm;
+    tn = (pid % (GM * Nt)) / gm;
+  };
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tm_a);
+    tma_prefetch(&tm_b);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 2 * BN);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol_w = l2_policy_evict_first(), pol_x = l2_policy_evict_last();
+      auto load_w = [&](int s, int tn, int kb) {
+        if (p.w_packed) {
+#pragma unroll
+          for (int h = 0; h < BN / BM; ++h)
+            tma_load_2d(sb + s * B_BYTES + h * TILE_BYTES, &tm_b, &full[s], 0,
+                        ((tn * (BN / BM) + h) * p.kb_total + kb) * BM, pol_w);
+        } else {
+          tma_load_2d(sb + s * B_BYTES, &tm_b, &full[s], kb * BK, tn * BN, pol_w);
+        }
+      };
+      auto load_x = [&](int s, int tm, int kb) { tma_load_2d(sa + s * A_BYTES, &tm_a, &full[s], kb * BK, tm * BM, pol_x); };
+      int i = 0;
+      bool first = true;
+      for (int pid = blockIdx.x; pid < tiles; pid += G) {
+        int tm, tn;
+        tile_mn(pid, tm, tn);
+        int kb = 0;
+        if (first) {  // the first tile's weight blocks go out before the dependency wait
+          const int pre = min(nkb, STAGES);
+          for (int j = 0; j < pre; ++j) {
+            mbar_arrive_expect_tx(&full[j], A_BYTES + B_BYTES);
+            load_w(j, tn, j);
+          }
+          pdl_wait();
+          for (int j = 0; j < pre; ++j) load_x(j, tm, j);
+          i = kb = pre;
+          first = false;
+        }
+        for (; kb < nkb; ++kb, ++i) {
+          const int s = i % STAGES;
+          mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+          mbar_arrive_expect_tx(&full[s], A_BYTES + B_BYTES);
+          load_w(s, tn, kb);
+          load_x(s, tm, kb);
+        }
+      }
+      if (first) pdl_wait();  // no tile (never: grid <= tiles), keep the PDL contract
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+      int i = 0, lt = 0;
+      for (int pid = blockIdx.x; pid < tiles; pid += G, ++lt) {
+        const int buf = lt & 1;
+        mbar_wait(&tempty[buf], ((lt >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t acc = tmem + buf * BN;
+        for (int kb = 0; kb < nkb; ++kb, ++i) {
+          const int s = i % STAGES;
+          mbar_wait(&full[s], (i / STAGES) & 1);
+          tc_fence_after();
+          const uint64_t ad = umma_desc_sw128(sa + s * A_BYTES);
+          const uint64_t bd = umma_desc_sw128(sb + s * B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk)
+            umma_bf16(acc, ad + 2 * kk, bd + 2 * kk, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&tfull[buf]);
+      }
+    }
+  } else {
+    // epilogue warps 2..5 -> TMEM lane quarters (warp % 4): tile rows
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const OutDesc od = out_of(p);
+    int lt = 0;
+    for (int pid = blockIdx.x; pid < tiles; pid += G, ++lt) {
+      int tm, tn;
+      tile_mn(pid, tm, tn);
+      const int buf = lt & 1;
+      mbar_wait(&tfull[buf], (lt >> 1) & 1);
+      tc_fence_after();
+      const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + buf * BN;
+      const int m = tm * BM + row;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 16) {
+        float v[16];
+        tmem_ld16(trow + c, v);
+        store_chunk(od, m, tn * BN + c, v);
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[buf]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, 2 * BN);
+}
+
 // ------------------------------------------------------------------ stream-K decode
 // Persistent weight-streaming GEMM for decode (A = weights, 128-row tiles;
 // B = the n_tok <= 64 activation rows). The tiles x K-blocks unit space is
@@ -1193,6 +1343,23 @@ static int linear_impl(const void *w, const void *x, void *y, int dtype, int y_d
     if (pl.tiles > kMaxTickets) return HX_ERR_UNSUPPORTED;
     p.counters = reinterpret_cast<int *>(workspace);
     p.ws = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(workspace) + kTicketBytes);
+  }
+  static const bool persistent = [] {  // HX_GEMM_PERSISTENT=0: one CTA per tile (round-1 kernel)
+    const char *e = getenv("HX_GEMM_PERSISTENT");
+    return e ? atoi(e) != 0 : true;
+  }();
+  if (persistent && pl.bn == 256 && pl.splits == 1 && p.epi.mode == EPI_PLAIN && !p.a_is_weight) {
+    constexpr int STG = 4;
+    const size_t smem = 1024 + STG * (BM * BK * 2 + 256 * BK * 2) + (2 * STG + 4) * 8 + 16;
+    static bool attr_done = false;
+    if (!attr_done) {
+      cudaFuncSetAttribute(gemm_tc_persistent_kernel<256, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+      attr_done = true;
+    }
+    const int tiles = ((p.M + BM - 1) / BM) * ((p.N + 255) / 256);
+    return launch(gemm_tc_persistent_kernel<256, STG>, dim3(std::min(tiles, kNumSMs)), dim3(192), smem, st, ma, mb,
+                  p);
   }
   switch (pl.bn) {
     case 16: return launch_tc<16, 6>(ma, mb, p, pl.splits, st);
