@@ -1348,7 +1348,11 @@ static int linear_impl(const void *w, const void *x, void *y, int dtype, int y_d
     const char *e = getenv("HX_GEMM_PERSISTENT");
     return e ? atoi(e) != 0 : true;
   }();
-  if (persistent && pl.bn == 256 && pl.splits == 1 && p.epi.mode == EPI_PLAIN && !p.a_is_weight) {
+  // measured: +4-10 % at the engine's prefill shapes (<= 4096 token rows; 7B / 13B
+  // prompts, 70B micro-batches of 2048 rows, up to ~3600 tiles), but -10-20 % on
+  // one-shot 32768-row GEMMs (>= 8192 tiles): there the per-tile kernel is kept
+  const int n_tiles = ((p.M + BM - 1) / BM) * ((p.N + 255) / 256);
+  if (persistent && pl.bn == 256 && pl.splits == 1 && p.epi.mode == EPI_PLAIN && !p.a_is_weight && n_tiles <= 4096) {
     constexpr int STG = 4;
     const size_t smem = 1024 + STG * (BM * BK * 2 + 256 * BK * 2) + (2 * STG + 4) * 8 + 16;
     static bool attr_done = false;
