@@ -101,27 +101,6 @@ int hx_linear(const void *w, const void *x, void *y, int dtype, int y_dtype,
               void *workspace, size_t workspace_bytes, hx_stream_t stream);
 size_t hx_linear_workspace(int dtype, int n_tok, int n_out, int k_dim);
 
-/* Fused-epilogue projections (bf16, n_out % 128 == 0). Output feature f < 64 of
- * every 128-wide group is paired with f + 64 in the epilogue, from the fp32
- * accumulators:
- *  - hx_linear_swiglu: w_gu rows interleaved in 64-row blocks [gate_g; up_g];
- *    act[t, 64 g + i] = silu(gate) * up (bf16, row pitch ld_act).
- *  - hx_linear_rope_kv: w_qkv = [q heads; k heads; v heads] x 128; RoPE
- *    (rotate-half, theta) on q and k, then q -> q_out [n_tok, hq, 128] and k, v
- *    -> the paged cache (same token/position rules as hx_rope_kv_append).
- * These replace hx_linear + hx_swiglu and hx_linear + hx_rope_kv_append. */
-int hx_linear_swiglu(const void *w_gu, const void *x, void *act, int ld_act, int n_tok, int n_out,
-                     int k_dim, int flags, void *workspace, size_t workspace_bytes, hx_stream_t stream);
-int hx_linear_rope_kv(const void *w_qkv, const void *x, void *q_out, void *k_cache, void *v_cache,
-                      const int32_t *block_table, const int32_t *seq_lens, int n_tok, int prefill_len,
-                      int hq, int hkv, int page_size, int max_blocks, float theta,
-                      const void *rope_table, int rope_table_len, int k_dim, int flags,
-                      void *workspace, size_t workspace_bytes, hx_stream_t stream);
-/* (cos, sin) of pos * theta^(-2i / (2 half)) for pos < max_pos, i < half, as
- * float2 [max_pos][half] -- the values the RoPE kernels compute, precomputed
- * (optional rope_table of hx_linear_rope_kv; NULL = compute inline). */
-int hx_rope_table(void *table, int max_pos, int half, float theta, hx_stream_t stream);
-
 /* Repack a bf16 weight [n_out, k_dim] into [ceil(n/128)][ceil(k/64)][128][64]
  * tiles (zero padded) so each 16 KB tile the decode GEMM streams is one
  * contiguous HBM range; packed holds hx_packed_weight_elems(n_out, k_dim). */

@@ -98,16 +98,10 @@ class Oracle:
     attention output, gate/up and SwiGLU outputs); the residual stream, the
     row-parallel outputs and logits stay fp32 as in the engine."""
 
-    def __init__(self, cfg, weights, act_bf16=False, fused=(True, True)):
+    def __init__(self, cfg, weights, act_bf16=False):
         self.cfg = cfg
         self.w = weights
         self.r = bf16_round if act_bf16 else (lambda a: a)
-        # the engine's fused GEMM epilogues (fused = (swiglu, rope)) round once, from
-        # the fp32 accumulators: RoPE'd q/k (128-wide heads) and silu(gate) * up are
-        # then never rounded before use
-        ident = lambda a: a  # noqa: E731
-        self.r_pre_rope = ident if (act_bf16 and fused[1] and cfg.head_dim == 128) else self.r
-        self.r_pre_swiglu = ident if (act_bf16 and fused[0]) else self.r
 
     def layer(self, l, x, pos0, cache):
         cfg, lw = self.cfg, self.w["layers"][l]
@@ -115,9 +109,8 @@ class Oracle:
         hd, hq, hkv = cfg.head_dim, cfg.num_heads, cfg.num_kv_heads
         r = self.r
         h = r(rmsnorm(x, lw["ln_attn"], cfg.rms_eps))
-        rp = self.r_pre_rope if s == 1 else r  # the engine fuses RoPE into the decode QKV GEMM only
-        q = rp(lin(h, lw["q"])).reshape(b, s, hq, hd).transpose(0, 2, 1, 3)
-        k = rp(lin(h, lw["k"])).reshape(b, s, hkv, hd).transpose(0, 2, 1, 3)
+        q = r(lin(h, lw["q"])).reshape(b, s, hq, hd).transpose(0, 2, 1, 3)
+        k = r(lin(h, lw["k"])).reshape(b, s, hkv, hd).transpose(0, 2, 1, 3)
         v = r(lin(h, lw["v"])).reshape(b, s, hkv, hd).transpose(0, 2, 1, 3)
         cos, sin = rope_tables(hd, cfg.rope_theta, np.arange(pos0, pos0 + s))
         q, k = r(apply_rope(q, cos, sin)), r(apply_rope(k, cos, sin))
@@ -130,8 +123,7 @@ class Oracle:
         o = o.transpose(0, 2, 1, 3).reshape(b, s, hq * hd)
         x = (x + lin(o, lw["o"])).astype(F32)
         h = r(rmsnorm(x, lw["ln_mlp"], cfg.rms_eps))
-        rs = self.r_pre_swiglu
-        a = r(silu(rs(lin(h, lw["gate"]))) * rs(lin(h, lw["up"])))  # silu in fp32, one rounding
+        a = r(silu(r(lin(h, lw["gate"]))) * r(lin(h, lw["up"])))  # silu in fp32, one rounding
         return (x + lin(a, lw["down"])).astype(F32)
 
     def logits(self, x_last):
@@ -250,8 +242,7 @@ def streamed_teacher_forced(cfg, seed, seq, positions, modes=((True, True), (Tru
     seeded streams as ``init_tensor`` (``weights.layer_stream``), used by every
     mode and dropped. Equivalent to prefill + teacher-forced decode steps (the
     layer math is per position except the causal attention; the engine stores
-    bf16 at the same points in both phases when the GEMM epilogues are
-    unfused). ``modes``: (weights rounded to bf16, activations rounded to bf16)
+    bf16 at the same points in both phases). ``modes``: (weights rounded to bf16, activations rounded to bf16)
     pairs; returns {mode: logits [len(positions), b, V]}."""
     from paper_2311_11514_b200.weights import init_globals, layer_stream
     seq = np.asarray(seq)
@@ -265,11 +256,11 @@ def streamed_teacher_forced(cfg, seed, seq, positions, modes=((True, True), (Tru
         if any(m[0] for m in modes):
             w[True] = {"layers": {l: {k: (v if k.startswith("ln_") else bf16_round(v)) for k, v in lw.items()}}}
         for m in modes:
-            xs[m] = Oracle(cfg, w[m[0]], act_bf16=m[1], fused=(False, False)).layer(l, xs[m], 0, Cache())
+            xs[m] = Oracle(cfg, w[m[0]], act_bf16=m[1]).layer(l, xs[m], 0, Cache())
         del w, lw
     pos = list(positions)
     out = {}
     for m in modes:
-        o = Oracle(cfg, glob[m[0]], act_bf16=m[1], fused=(False, False))
+        o = Oracle(cfg, glob[m[0]], act_bf16=m[1])
         out[m] = np.stack([o.logits(xs[m][:, p]) for p in pos], 0)
     return out

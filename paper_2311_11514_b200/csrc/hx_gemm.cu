@@ -37,23 +37,6 @@ constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle row
 constexpr int kNumSMs = 148;
 constexpr uint32_t TILE_BYTES = BM * BK * 2;  // one packed 128x64 weight tile
 
-// Fused epilogues. Both pair output feature f (< 64 within a 128-wide group)
-// with f + 64 of the same group: the interleaved gate/up weight layout puts
-// gate rows [64g, 64g+64) next to the matching up rows, and rotate-half RoPE
-// pairs element i with i + 64 of a 128-wide head.
-enum EpiMode { EPI_PLAIN = 0, EPI_SWIGLU = 1, EPI_ROPE_KV = 2 };
-struct EpiArgs {
-  int mode;
-  __nv_bfloat16 *act;  // SWIGLU: [n_tok][n_out / 2], row pitch ld_act
-  long ld_act;
-  __nv_bfloat16 *q_out, *k_cache, *v_cache;  // ROPE_KV (bf16, hd = 128)
-  const int32_t *bt, *seq_lens;
-  int hq, hkv, page, max_blocks, prefill_len;
-  float theta;
-  const float2 *rope_tab;  // optional [max_pos][64] (cos, sin) from hx_rope_table; else computed
-  int rope_tab_len;
-};
-
 struct GemmArgs {
   void *c;
   long ldm, ldn;  // C[m * ldm + n * ldn]
@@ -66,52 +49,7 @@ struct GemmArgs {
   int w_packed;
   float *ws;
   int *counters;
-  EpiArgs epi;
 };
-
-// token -> (sequence, position) for the RoPE/KV epilogue (decode: one token per sequence)
-__device__ __forceinline__ void tok_pos(const EpiArgs &e, int tok, int &b, int &pos) {
-  b = e.prefill_len ? tok / e.prefill_len : tok;
-  pos = e.seq_lens[b] + (e.prefill_len ? tok % e.prefill_len : 0);
-}
-
-// one output element pair of the fused epilogues: feature n (< 64 in its
-// 128-group) with value lo, partner n + 64 with value hi, for token tok
-__device__ __forceinline__ void epi_pair(const EpiArgs &e, int tok, int n, float lo, float hi) {
-  if (e.mode == EPI_SWIGLU) {
-    const int f = (n >> 7) * 64 + (n & 63);  // activation feature
-    e.act[(long)tok * e.ld_act + f] = __float2bfloat16_rn((lo / (1.0f + expf(-lo))) * hi);
-    return;
-  }
-  const int h = n >> 7, i = n & 63;
-  int b, pos;
-  tok_pos(e, tok, b, pos);
-  float y1 = lo, y2 = hi;
-  if (h < e.hq + e.hkv) {  // q and k heads: rotate-half RoPE, fp32 accumulator in
-    float sn, cs;
-    if (e.rope_tab && pos < e.rope_tab_len) {  // same fp32 values, precomputed
-      const float2 t = e.rope_tab[(long)pos * 64 + i];
-      cs = t.x;
-      sn = t.y;
-    } else {
-      const float inv_freq = 1.0f / powf(e.theta, (float)(2 * i) / 128.0f);
-      sincosf((float)pos * inv_freq, &sn, &cs);
-    }
-    const float2 y = rope_rot(lo, hi, cs, sn);
-    y1 = y.x;
-    y2 = y.y;
-  }
-  __nv_bfloat16 *dst;
-  if (h < e.hq) {
-    dst = e.q_out + ((long)tok * e.hq + h) * 128;
-  } else {
-    const int kvh = (h < e.hq + e.hkv) ? h - e.hq : h - e.hq - e.hkv;
-    const int blk = e.bt[(long)b * e.max_blocks + pos / e.page];
-    dst = (h < e.hq + e.hkv ? e.k_cache : e.v_cache) + (((long)blk * e.hkv + kvh) * e.page + pos % e.page) * 128;
-  }
-  dst[i] = __float2bfloat16_rn(y1);
-  dst[i + 64] = __float2bfloat16_rn(y2);
-}
 
 // plain output descriptor, passed by value (registers): C[m * ldm + n * ldn]
 struct OutDesc {
@@ -267,33 +205,7 @@ __global__ void __launch_bounds__(128, 1)
   const int row = warp * 32 + lane;
   const int m = m0 + row;
   const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
-  if (splits == 1 && p.epi.mode != EPI_PLAIN) {
-    // prefill orientation: this thread owns token row m; feature pairs (c, c + 64)
-    // of each 128-wide group sit in its own registers -- no exchange needed
-#pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 128) {
-#pragma unroll 1
-      for (int c = c0; c < c0 + 64; c += 16) {
-        float lo[16], hi[16];
-        tmem_ld16(trow + c, lo);
-        tmem_ld16(trow + c + 64, hi);
-        if (m < p.M && n0 + c0 < p.N) {
-          if (p.epi.mode == EPI_SWIGLU) {  // 16 consecutive activations: two 16-byte stores
-            float a[16];
-#pragma unroll
-            for (int j = 0; j < 16; ++j) a[j] = (lo[j] / (1.0f + expf(-lo[j]))) * hi[j];
-            const int f = ((n0 + c) >> 7) * 64 + ((n0 + c) & 63);
-            __nv_bfloat16 *dst = p.epi.act + (long)m * p.epi.ld_act + f;
-            Vec16<__nv_bfloat16>::store(dst, a);
-            Vec16<__nv_bfloat16>::store(dst + 8, a + 8);
-          } else {
-#pragma unroll 1
-            for (int j = 0; j < 16; ++j) epi_pair(p.epi, m, n0 + c + j, lo[j], hi[j]);
-          }
-        }
-      }
-    }
-  } else if (splits == 1) {
+  if (splits == 1) {
 #pragma unroll 1
     for (int c = 0; c < BN; c += 16) {
       float v[16];
@@ -515,7 +427,6 @@ struct SKArgs {
   unsigned long long *trace;  // optional per-CTA timeline (hx_debug_trace): start, wait done, end, smid
   int l2pf;                   // weight tiles beyond the smem ring prefetched into L2 before the PDL wait
   const uint8_t *w_ptr;       // packed weights (for the epilogue warps' L2 prefetch)
-  EpiArgs epi;
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -530,88 +441,8 @@ __device__ __forceinline__ unsigned smid() {
 }
 
 // c * units < 2^31 for every decode shape (units <= 4096 tiles x 172 K-blocks, G <= 296)
-// (cos, sin)(pos * inv_freq_i), i < half, exactly as the RoPE kernels compute them
-__global__ void rope_table_kernel(float2 *tab, int max_pos, int half, float theta) {
-  pdl_trigger();
-  pdl_wait();
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= max_pos * half) return;
-  const int pos = idx / half, i = idx % half;
-  const float inv_freq = 1.0f / powf(theta, (float)(2 * i) / (float)(2 * half));
-  float sn, cs;
-  sincosf((float)pos * inv_freq, &sn, &cs);
-  tab[idx] = make_float2(cs, sn);
-}
 
-// decode-orientation output of one epilogue thread: feature row m of the tile,
-// 16 token columns starting at cc. The fused modes pair row r (< 64) with row
-// r + 64 through smem; all 128 epilogue threads must call this together.
-template <bool FUSED>
-__device__ __forceinline__ void emit_decode(const OutDesc od, const EpiArgs &epi, float *xch, int row, int m,
-                                            int cc, const float *v) {
-  if (!FUSED) {
-    store_chunk(od, m, cc, v);
-    return;
-  }
-  named_bar_sync(2, 128);  // previous exchange fully consumed
-#pragma unroll
-  for (int j = 0; j < 16; ++j) xch[row * 17 + j] = v[j];
-  named_bar_sync(2, 128);
-  if (row >= 64 || m >= od.M) return;
-  const int i = row;  // pair index within the 128-group (tile = one group)
-  if (epi.mode == EPI_SWIGLU) {
-    const int f = (m >> 7) * 64 + i;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const float lo = v[j], hi = xch[(row + 64) * 17 + j];
-      if (cc + j < od.N) epi.act[(long)(cc + j) * epi.ld_act + f] = __float2bfloat16_rn((lo / (1.0f + expf(-lo))) * hi);
-    }
-    return;
-  }
-  // RoPE/KV, four tokens at a time: the position, page and cos/sin loads of a
-  // group are all issued before any use; both halves of the pair come from smem
-  const int h = m >> 7;
-  const bool rot = h < epi.hq + epi.hkv;
-  const bool tab = rot && epi.rope_tab != nullptr;
-#pragma unroll 1
-  for (int j0 = 0; j0 < 16; j0 += 4) {
-    int pos[4], blk[4];
-    float2 cs[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) pos[j] = epi.seq_lens[min(cc + j0 + j, od.N - 1)];  // decode: token = sequence
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int tok = min(cc + j0 + j, od.N - 1);
-      blk[j] = h < epi.hq ? 0 : epi.bt[(long)tok * epi.max_blocks + pos[j] / epi.page];
-      cs[j] = (tab && pos[j] < epi.rope_tab_len) ? epi.rope_tab[(long)pos[j] * 64 + i] : make_float2(1.f, 0.f);
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int tok = cc + j0 + j;
-      if (tok >= od.N) break;
-      const float lo = xch[row * 17 + j0 + j], hi = xch[(row + 64) * 17 + j0 + j];
-      float c = cs[j].x, s = cs[j].y;
-      if (rot && !(tab && pos[j] < epi.rope_tab_len)) {
-        const float inv_freq = 1.0f / powf(epi.theta, (float)(2 * i) / 128.0f);
-        sincosf((float)pos[j] * inv_freq, &s, &c);
-      }
-      const float2 y = rot ? rope_rot(lo, hi, c, s) : make_float2(lo, hi);
-      const float y1 = y.x, y2 = y.y;
-      __nv_bfloat16 *dst;
-      if (h < epi.hq) {
-        dst = epi.q_out + ((long)tok * epi.hq + h) * 128;
-      } else {
-        const int kvh = rot ? h - epi.hq : h - epi.hq - epi.hkv;
-        dst = (rot ? epi.k_cache : epi.v_cache) + (((long)blk[j] * epi.hkv + kvh) * epi.page + pos[j] % epi.page) * 128;
-      }
-      dst[i] = __float2bfloat16_rn(y1);
-      dst[i + 64] = __float2bfloat16_rn(y2);
-    }
-  }
-}
-
-
-template <int BN, int STAGES, bool FUSED>
+template <int BN, int STAGES>
 __global__ void __launch_bounds__(192, 2)
     gemm_streamk_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
                         const __grid_constant__ SKArgs p) {
@@ -627,7 +458,6 @@ __global__ void __launch_bounds__(192, 2)
   uint64_t *tfull = empty + STAGES;   // [2]
   uint64_t *tempty = tfull + 2;       // [2]
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
-  float *xch = reinterpret_cast<float *>(tempty + 4);  // [128][17] pair exchange for the fused epilogues
   __shared__ int s_last;
 
   pdl_trigger();
@@ -748,7 +578,7 @@ __global__ void __launch_bounds__(192, 2)
         float v[16];
         tmem_ld16(tacc + cc, v);
         if (whole) {
-          emit_decode<FUSED>(ga, p.epi, xch, row, m, cc, v);
+          store_chunk(ga, m, cc, v);
         } else {
 #pragma unroll
           for (int j = 0; j < 16; ++j) __stcg(mine + (size_t)(cc + j) * BM, v[j]);
@@ -800,7 +630,7 @@ __global__ void __launch_bounds__(192, 2)
               }
             }
           }
-          emit_decode<FUSED>(ga, p.epi, xch, row, m, ch, acc);
+          store_chunk(ga, m, ch, acc);
         }
       }
     }
@@ -1111,22 +941,21 @@ extern "C" size_t hx_linear_workspace(int dtype, int n_tok, int n_out, int k_dim
   return kTicketBytes + (size_t)pl.tiles * pl.splits * BM * pl.bn * sizeof(float);
 }
 
-template <int BN, int STAGES, bool FUSED = false>
+template <int BN, int STAGES>
 static int launch_sk(const CUtensorMap &mw, const CUtensorMap &mx, const SKArgs &p, cudaStream_t st) {
-  // The pair-exchange buffer only exists in the fused instantiations. The request
-  // is floored at just over half an SM's shared memory so that exactly one
-  // stream-K CTA lands on every SM: when two fit, the block scheduler may stack
-  // two CTAs of the same launch on one SM (measured +0.11 ms per 7B decode step).
-  // Smaller kernels (norms, attention) still co-reside under PDL.
+  // The request is floored at just over half an SM's shared memory so that
+  // exactly one stream-K CTA lands on every SM: when two fit, the block
+  // scheduler may stack two CTAs of the same launch on one SM (measured +0.11
+  // ms per 7B decode step). Smaller kernels (norms, attention) still co-reside
+  // under PDL.
   const size_t kOneCtaPerSm = sk_ctas() > kNumSMs ? 0 : 116 * 1024;
-  const size_t smem = std::max<size_t>(kOneCtaPerSm, 1024 + STAGES * (BM * BK * 2 + BN * BK * 2) + (2 * STAGES + 4) * 8 + 32 +
-                                                 (FUSED ? 128 * 17 * 4 : 0));
+  const size_t smem = std::max<size_t>(kOneCtaPerSm, 1024 + STAGES * (BM * BK * 2 + BN * BK * 2) + (2 * STAGES + 4) * 8 + 32);
   static bool attr_done = false;
   if (!attr_done) {
-    cudaFuncSetAttribute(gemm_streamk_kernel<BN, STAGES, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(gemm_streamk_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr_done = true;
   }
-  return launch(gemm_streamk_kernel<BN, STAGES, FUSED>, dim3(sk_grid(p.units)), dim3(192), smem, st, mw, mx, p);
+  return launch(gemm_streamk_kernel<BN, STAGES>, dim3(sk_grid(p.units)), dim3(192), smem, st, mw, mx, p);
 }
 
 namespace hx {
@@ -1201,67 +1030,10 @@ extern "C" int hx_pack_weight(const void *w, void *packed, int n_out, int k_dim,
                 (__nv_bfloat16 *)packed, n_out, k_dim, KB);
 }
 
-static int linear_impl(const void *w, const void *x, void *y, int dtype, int y_dtype, int n_tok, int n_out,
-                       int k_dim, int ldy, int flags, void *workspace, size_t workspace_bytes, hx_stream_t stream,
-                       const EpiArgs &epi);
-
-extern "C" int hx_linear(const void *w, const void *x, void *y, int dtype, int y_dtype, int n_tok,
-                         int n_out, int k_dim, int ldy, int flags, void *workspace,
-                         size_t workspace_bytes, hx_stream_t stream) {
-  EpiArgs epi{};
-  return linear_impl(w, x, y, dtype, y_dtype, n_tok, n_out, k_dim, ldy, flags, workspace, workspace_bytes, stream,
-                     epi);
-}
-
-extern "C" int hx_linear_swiglu(const void *w_gu, const void *x, void *act, int ld_act, int n_tok, int n_out,
-                                int k_dim, int flags, void *workspace, size_t workspace_bytes, hx_stream_t stream) {
-  if (!act || n_out % 128 || ld_act < n_out / 2 || (flags & (HX_LINEAR_ACCUMULATE | HX_LINEAR_DEFER_REDUCE)))
-    return HX_ERR_ARG;
-  EpiArgs epi{};
-  epi.mode = EPI_SWIGLU;
-  epi.act = reinterpret_cast<__nv_bfloat16 *>(act);
-  epi.ld_act = ld_act;
-  return linear_impl(w_gu, x, nullptr, HX_BF16, HX_BF16, n_tok, n_out, k_dim, n_out, flags, workspace,
-                     workspace_bytes, stream, epi);
-}
-
-extern "C" int hx_rope_table(void *table, int max_pos, int half, float theta, hx_stream_t stream) {
-  if (!table || max_pos <= 0 || half <= 0) return HX_ERR_ARG;
-  const int n = max_pos * half;
-  return launch(rope_table_kernel, dim3((n + 255) / 256), dim3(256), 0, as_stream(stream),
-                reinterpret_cast<float2 *>(table), max_pos, half, theta);
-}
-
-extern "C" int hx_linear_rope_kv(const void *w_qkv, const void *x, void *q_out, void *k_cache, void *v_cache,
-                                 const int32_t *block_table, const int32_t *seq_lens, int n_tok, int prefill_len,
-                                 int hq, int hkv, int page_size, int max_blocks, float theta, const void *rope_table,
-                                 int rope_table_len, int k_dim, int flags, void *workspace, size_t workspace_bytes,
-                                 hx_stream_t stream) {
-  if (!q_out || !k_cache || !v_cache || !block_table || !seq_lens || page_size <= 0 ||
-      (flags & (HX_LINEAR_ACCUMULATE | HX_LINEAR_DEFER_REDUCE)))
-    return HX_ERR_ARG;
-  EpiArgs epi{};
-  epi.mode = EPI_ROPE_KV;
-  epi.q_out = reinterpret_cast<__nv_bfloat16 *>(q_out);
-  epi.k_cache = reinterpret_cast<__nv_bfloat16 *>(k_cache);
-  epi.v_cache = reinterpret_cast<__nv_bfloat16 *>(v_cache);
-  epi.bt = block_table;
-  epi.seq_lens = seq_lens;
-  epi.hq = hq; epi.hkv = hkv; epi.page = page_size; epi.max_blocks = max_blocks;
-  epi.prefill_len = prefill_len; epi.theta = theta;
-  epi.rope_tab = reinterpret_cast<const float2 *>(rope_table);
-  epi.rope_tab_len = rope_table ? rope_table_len : 0;
-  const int n_out = (hq + 2 * hkv) * 128;
-  return linear_impl(w_qkv, x, nullptr, HX_BF16, HX_BF16, n_tok, n_out, k_dim, n_out, flags, workspace,
-                     workspace_bytes, stream, epi);
-}
-
-static int linear_impl(const void *w, const void *x, void *y, int dtype, int y_dtype, int n_tok, int n_out,
-                       int k_dim, int ldy, int flags, void *workspace, size_t workspace_bytes, hx_stream_t stream,
-                       const EpiArgs &epi) {
+extern "C" int hx_linear(const void *w, const void *x, void *y, int dtype, int y_dtype, int n_tok, int n_out,
+                         int k_dim, int ldy, int flags, void *workspace, size_t workspace_bytes, hx_stream_t stream) {
   if (n_tok <= 0 || n_out <= 0 || k_dim <= 0) return n_tok == 0 ? 0 : HX_ERR_ARG;
-  if (!w || !x || (epi.mode == EPI_PLAIN && (!y || ldy < n_out))) return HX_ERR_ARG;
-  if (epi.mode != EPI_PLAIN && (dtype != HX_BF16 || n_out % 128)) return HX_ERR_UNSUPPORTED;
+  if (!w || !x || !y || ldy < n_out) return HX_ERR_ARG;
   const int accumulate = flags & HX_LINEAR_ACCUMULATE;
   const int packed = (flags & HX_LINEAR_PACKED) ? 1 : 0;
   cudaStream_t st = as_stream(stream);
@@ -1279,7 +1051,6 @@ static int linear_impl(const void *w, const void *x, void *y, int dtype, int y_d
   p.c = y;
   p.K = k_dim;
   p.c_bf16 = (y_dtype == HX_BF16);
-  p.epi = epi;
   p.accumulate = accumulate;
   p.kb_total = (k_dim + BK - 1) / BK;
   p.kb_per_split = pl.kb_per;
@@ -1303,7 +1074,7 @@ static int linear_impl(const void *w, const void *x, void *y, int dtype, int y_d
     sk.l2pf = ((flags & HX_LINEAR_L2_PREFETCH) || l2pf_all) ? l2pf : 0;
     sk.w_ptr = reinterpret_cast<const uint8_t *>(w);
     sk.c = y; sk.ldm = 1; sk.ldn = ldy; sk.M = n_out; sk.N = n_tok;
-    sk.c_bf16 = p.c_bf16; sk.accumulate = accumulate; sk.w_packed = packed; sk.epi = epi;
+    sk.c_bf16 = p.c_bf16; sk.accumulate = accumulate; sk.w_packed = packed;
     sk.defer = (flags & HX_LINEAR_DEFER_REDUCE) ? 1 : 0;
     if (sk.defer && (p.c_bf16 || accumulate)) return HX_ERR_UNSUPPORTED;
     sk.KB = p.kb_total; sk.units = pl.tiles * p.kb_total;
@@ -1316,13 +1087,6 @@ static int linear_impl(const void *w, const void *x, void *y, int dtype, int y_d
     if (g_trace && g_trace_pos + g <= g_trace_cap) {
       sk.trace = g_trace + 8 * g_trace_pos;
       g_trace_pos += g;
-    }
-    if (p.epi.mode != EPI_PLAIN) {  // fused epilogues: separate instantiations keep the plain kernel spill-free
-      switch (pl.bn) {
-        case 16: return launch_sk<16, 6, true>(ma, mb, sk, st);
-        case 32: return launch_sk<32, 5, true>(ma, mb, sk, st);
-        default: return launch_sk<64, 4, true>(ma, mb, sk, st);
-      }
     }
     // ring depths 6 / 5 / 4 (BN 16 / 32 / 64): deeper rings (HX_SK_STAGES 8-12,
     // HX_SK32_STAGES 7-9 in round 1) measured neutral and were dropped
@@ -1352,7 +1116,7 @@ static int linear_impl(const void *w, const void *x, void *y, int dtype, int y_d
   // prompts, 70B micro-batches of 2048 rows, up to ~3600 tiles), but -10-20 % on
   // one-shot 32768-row GEMMs (>= 8192 tiles): there the per-tile kernel is kept
   const int n_tiles = ((p.M + BM - 1) / BM) * ((p.N + 255) / 256);
-  if (persistent && pl.bn == 256 && pl.splits == 1 && p.epi.mode == EPI_PLAIN && !p.a_is_weight && n_tiles <= 4096) {
+  if (persistent && pl.bn == 256 && pl.splits == 1 && !p.a_is_weight && n_tiles <= 4096) {
     constexpr int STG = 4;
     const size_t smem = 1024 + STG * (BM * BK * 2 + 256 * BK * 2) + (2 * STG + 4) * 8 + 16;
     static bool attr_done = false;

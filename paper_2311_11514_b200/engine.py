@@ -43,14 +43,6 @@ from .weights import _CODES, LAYER_TENSORS, init_globals, layer_stream, shard_la
 DTYPES = {"bf16": torch.bfloat16, "fp32": torch.float32}
 
 
-def fused_epilogues() -> tuple[bool, bool]:
-    """(SwiGLU-in-gate/up-GEMM, RoPE+KV-append-in-decode-QKV-GEMM) for the bf16
-    tensor-core path; off by default (measured slower than the separate kernels at
-    7B batch 16), HX_FUSE_SWIGLU=1 / HX_FUSE_ROPE=1 enable them.
-    The bf16 oracle takes the same pair (rounding points differ between the two)."""
-    return (os.environ.get("HX_FUSE_SWIGLU", "0") == "1", os.environ.get("HX_FUSE_ROPE", "0") == "1")
-
-
 # --------------------------------------------------------------------- weights
 def _device_tensor(cfg, seed, name, layer, device):
     """Synthetic weights generated on the device (fast path for large models):
@@ -181,24 +173,15 @@ class RankExecutor:
         self.cfg, self.role, self.dtype, self.device = cfg, role, dtype, torch.device(device)
         self.k = kernels or _ops
         self.w = weights
-        inter_r = cfg.intermediate // role.tp
-        # fused GEMM epilogues (bf16 tensor-core path): SwiGLU needs 64-row gate/up
-        # blocks, RoPE+KV-append needs 128-wide heads
-        tc = pack_weights and dtype == torch.bfloat16 and self.device.type == "cuda" and self.k is _ops
-        want_swiglu, want_rope = fused_epilogues()
-        self.fuse_swiglu = tc and want_swiglu and inter_r % 64 == 0
-        self.fuse_rope = tc and want_rope and cfg.head_dim == 128
         # decode RoPE + KV append inside the TMA attention kernel (bit-identical to
         # the separate kernels); HX_FUSE_ROPE_ATTN=0 selects rope_kv_append + attn_decode
-        self.rope_in_attn = (self.device.type == "cuda" and self.k is _ops and not self.fuse_rope
+        self.rope_in_attn = (self.device.type == "cuda" and self.k is _ops
                              and _ops.decode_rope_fusable(dtype, cfg.head_dim, page_size, cfg.num_heads // role.tp,
                                                           cfg.num_kv_heads // role.tp)
                              and os.environ.get("HX_FUSE_ROPE_ATTN", "1") != "0")
         if pack_weights and dtype == torch.bfloat16 and self.device.type == "cuda":
             # tile-contiguous layout for the weight-streaming GEMM (hx_pack_weight)
             for lw in weights["layers"]:
-                if self.fuse_swiglu:
-                    lw["wgu"] = _ops.interleave_gate_up(lw["wgu"])
                 for name in ("wqkv", "wo", "wgu", "wdown"):
                     lw[name] = _ops.PackedWeight(lw[name])
             if "lm_head" in weights:
@@ -248,7 +231,6 @@ class RankExecutor:
         self.defer = (tp == 1 and dtype == torch.bfloat16 and dev.type == "cuda" and self.k is _ops
                       and defer_reduce)
         self._defer_now = False
-        self.rope_tab = _ops.rope_table(self.max_ctx, self.hd, cfg.rope_theta, dev) if self.fuse_rope else None
         self.par = None          # ops.PeerAllReduce when TP>1 ranks run in separate processes
         self.stream = None       # this emulated rank's stream (Engine(local_peer=True))
         self._peer_now = False
@@ -270,7 +252,7 @@ class RankExecutor:
         # HX_DEFER_GU=0 / 1 forces it off / on.
         env = os.environ.get("HX_DEFER_GU")
         few_tiles = 2 * self.inter // 128 < 2 * 148
-        self.defer_gu = (dtype == torch.bfloat16 and dev.type == "cuda" and self.k is _ops and not self.fuse_swiglu
+        self.defer_gu = (dtype == torch.bfloat16 and dev.type == "cuda" and self.k is _ops
                          and (env == "1" or (env is None and few_tiles)))
         self.gu32 = z(batch, 2 * self.inter, dt=torch.float32) if self.defer_gu else None
         self._x_full = self.x
@@ -302,9 +284,6 @@ class RankExecutor:
             k.linear(lw["wqkv"], self.h, self.qkv, n_tok, self.lin_ws, **pf)
             k.attn_decode_rope_append(self.qkv, kc, vc, self.bt, self.sl, self.attn, n_tok,
                                       self.hq, self.hkv, self.hd, self.max_ctx, cfg.rope_theta, self.attn_ws)
-        elif self.fuse_rope and not prefill_len:  # decode: QKV GEMM with RoPE + KV append in its epilogue
-            k.linear_rope_kv(lw["wqkv"], self.h, self.q, kc, vc, self.bt, self.sl, n_tok,
-                             prefill_len, self.hq, self.hkv, cfg.rope_theta, self.lin_ws, self.rope_tab)
         else:
             k.linear(lw["wqkv"], self.h, self.qkv, n_tok, self.lin_ws)
             k.rope_kv_append(self.qkv, self.q, kc, vc, self.bt, self.sl, n_tok,
@@ -361,9 +340,7 @@ class RankExecutor:
 
     def mlp_body(self, li: int, n_tok: int):
         k, lw = self.k, self.w["layers"][li]
-        if self.fuse_swiglu:  # gate/up GEMM with SwiGLU in its epilogue (weights interleaved)
-            k.linear_swiglu(lw["wgu"], self.h, self.a, n_tok, self.lin_ws)
-        elif self.defer_gu and n_tok <= 64 and self._decode_now:
+        if self.defer_gu and n_tok <= 64 and self._decode_now:
             k.linear(lw["wgu"], self.h, self.gu32, n_tok, self.lin_ws, defer_reduce=True, **self._l2pf(0))
             k.splitk_swiglu(self.gu32, self.lin_ws, n_tok, self.cfg.hidden_dim, self.a)
         else:

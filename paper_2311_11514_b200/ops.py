@@ -38,10 +38,6 @@ _SIGS = {
     "hx_set_pdl": ([_I], None),
     "hx_debug_trace": ([_P, _SZ], _SZ),
     "hx_splitk_residual_rmsnorm": ([_P, _P, _I, _P, _I, _I, _I, _P, _P, _I, _F, _P], _I),
-    "hx_linear_swiglu": ([_P, _P, _P, _I, _I, _I, _I, _I, _P, _SZ, _P], _I),
-    "hx_linear_rope_kv": ([_P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _F, _P, _I, _I, _I, _P, _SZ, _P],
-                          _I),
-    "hx_rope_table": ([_P, _I, _I, _F, _P], _I),
     "hx_ipc_alloc": ([ctypes.POINTER(ctypes.c_void_p), _SZ], _I),
     "hx_ipc_free": ([_P], _I),
     "hx_ipc_handle": ([_P, ctypes.c_char_p], _I),
@@ -214,51 +210,6 @@ def linear(w, x, y, n_tok, workspace=None, accumulate=False, defer_reduce=False,
                             n_out, k, y.shape[-1], flags, _p(ws),
                             0 if ws is None else ws.numel() * ws.element_size(), _stream()),
            "hx_linear")
-
-
-def _wflags(w):
-    return (HX_LINEAR_PACKED, w.data) if isinstance(w, PackedWeight) else (0, w)
-
-
-def _wsz(ws):
-    return 0 if ws is None else ws.numel() * ws.element_size()
-
-
-def linear_swiglu(w_gu, x, act, n_tok, workspace=None):
-    """act = silu(x @ gate^T) * (x @ up^T) with w_gu rows interleaved in 64-row
-    [gate; up] blocks (interleave_gate_up), fused into the GEMM epilogue."""
-    n_out, k = w_gu.shape
-    flags, wp = _wflags(w_gu)
-    _check(load().hx_linear_swiglu(_p(wp), _p(x), _p(act), act.shape[-1], n_tok, n_out, k, flags, _p(workspace),
-                                   _wsz(workspace), _stream()), "hx_linear_swiglu")
-
-
-def linear_rope_kv(w_qkv, x, q_out, k_cache, v_cache, block_table, seq_lens, n_tok, prefill_len, hq, hkv,
-                   theta, workspace=None, rope_table=None):
-    """QKV projection with RoPE and the paged-KV append fused into the epilogue (hd 128)."""
-    n_out, k = w_qkv.shape
-    flags, wp = _wflags(w_qkv)
-    tab_len = rope_table.shape[0] if rope_table is not None else 0
-    _check(load().hx_linear_rope_kv(_p(wp), _p(x), _p(q_out), _p(k_cache), _p(v_cache), _p(block_table),
-                                    _p(seq_lens), n_tok, prefill_len, hq, hkv, k_cache.shape[2],
-                                    block_table.shape[1], theta, _p(rope_table), tab_len, k, flags,
-                                    _p(workspace), _wsz(workspace), _stream()), "hx_linear_rope_kv")
-
-
-def rope_table(max_pos, head_dim, theta, device="cuda"):
-    """[max_pos, head_dim // 2, 2] fp32 (cos, sin) table for the fused RoPE epilogue."""
-    t = torch.empty(max_pos, head_dim // 2, 2, dtype=torch.float32, device=device)
-    _check(load().hx_rope_table(_p(t), max_pos, head_dim // 2, theta, _stream()), "hx_rope_table")
-    return t
-
-
-def interleave_gate_up(wgu: torch.Tensor, block: int = 64) -> torch.Tensor:
-    """[gate; up] (2I x H) -> rows interleaved in `block`-row groups [gate_g; up_g]."""
-    two_i, h = wgu.shape
-    inter = two_i // 2
-    g = wgu[:inter].reshape(inter // block, block, h)
-    u = wgu[inter:].reshape(inter // block, block, h)
-    return torch.stack([g, u], dim=1).reshape(two_i, h).contiguous()
 
 
 def splitk_swiglu(y, workspace, n_tok, k_dim, out):

@@ -17,7 +17,7 @@ from oracle.llama_oracle import Oracle, bf16_weights
 from oracle.parity import bf16_verdict
 from paper_2311_11514_b200 import ops
 from paper_2311_11514_b200.config import LlamaConfig, TINY, preset
-from paper_2311_11514_b200.engine import Engine, fused_epilogues
+from paper_2311_11514_b200.engine import Engine
 from paper_2311_11514_b200.plan import simple_plan
 from paper_2311_11514_b200.weights import init_host_weights, synthetic_prompts
 
@@ -66,7 +66,7 @@ def _bf16_check(cfg, tps, layers, b, s, s_out, page=64, local_peer=False):
     positions with fp32 margin > 1e-2, and the first free-running divergence."""
     w = bf16_weights(init_host_weights(cfg, 0))
     prompt = synthetic_prompts(cfg, b, s, seed=1)
-    ids_o, lg_o = Oracle(cfg, w, act_bf16=True, fused=fused_epilogues()).generate(prompt, s_out)
+    ids_o, lg_o = Oracle(cfg, w, act_bf16=True).generate(prompt, s_out)
     eng = Engine(simple_plan(tps, layers), cfg, dtype="bf16", batch=b, max_prompt=s, max_out=s_out,
                  device="cuda:0", page_size=page, local_peer=local_peer)
     r = eng.generate(prompt, s_out, forced=ids_o)
@@ -82,14 +82,8 @@ def test_tiny_bf16_tolerance():
     _bf16_check(TINY, [2, 1], [3, 1], 2, 64, 16, page=16)
 
 
-FUSIONS = [pytest.param(("0", "0"), id="unfused"), pytest.param(("1", "1"), id="fused-epilogues")]
-
-
-@pytest.mark.parametrize("fuse", FUSIONS)
-def test_llama7b_shape_bf16_two_layers(fuse, monkeypatch):
+def test_llama7b_shape_bf16_two_layers():
     """Real 7B widths (H 4096, 32 heads, I 11008, V 32000) with 2 layers, b=8."""
-    monkeypatch.setenv("HX_FUSE_SWIGLU", fuse[0])
-    monkeypatch.setenv("HX_FUSE_ROPE", fuse[1])
     cfg = preset("llama2-7b", num_layers=2)
     _bf16_check(cfg, [1], [2], 8, 64, 6)
 
@@ -102,11 +96,8 @@ def test_llama7b_shape_bf16_tcgen05_prefill_attention(monkeypatch):
 
 
 @pytest.mark.parametrize("local_peer", [False, True], ids=["torch-sum", "peer-kernels"])
-@pytest.mark.parametrize("fuse", FUSIONS)
-def test_gqa_asymmetric_bf16(fuse, local_peer, monkeypatch):
+def test_gqa_asymmetric_bf16(local_peer):
     """GQA group 8 per rank (70B-style head ratio) under an asymmetric [2,1] plan."""
-    monkeypatch.setenv("HX_FUSE_SWIGLU", fuse[0])
-    monkeypatch.setenv("HX_FUSE_ROPE", fuse[1])
     cfg = LlamaConfig("gqa-mini", 2, 2048, 16, 2, 5632, 32000)
     _bf16_check(cfg, [2, 1], [1, 1], 4, 80, 6, page=32, local_peer=local_peer)
 
@@ -148,7 +139,6 @@ def test_llama7b_full_depth_c2():
       oracle does (one position of slack)."""
     from oracle.llama_oracle import streamed_teacher_forced
     from oracle.parity import rel_err, top2_margin
-    assert fused_epilogues() == (False, False)
     cfg = preset("llama2-7b")
     b, s, k = 8, 512, 4
     prompt = synthetic_prompts(cfg, b, s, seed=1)

@@ -144,47 +144,6 @@ def test_deferred_splitk_matches_in_kernel_reduction(n_tok, H, k):
     assert torch.equal(x2[n_tok:], x0[n_tok:])
 
 
-@pytest.mark.parametrize("n_tok,inter,k", [(8, 11008, 4096), (300, 768, 256), (33, 2816, 2048), (4096, 1408, 512)])
-def test_linear_swiglu_fused(n_tok, inter, k):
-    g = torch.Generator(device=DEV).manual_seed(inter + n_tok)
-    wgu = (torch.randn(2 * inter, k, device=DEV, generator=g) * 0.05).bfloat16()
-    x = torch.randn(n_tok, k, device=DEV, generator=g).bfloat16()
-    ws = torch.zeros(ops.linear_workspace(torch.bfloat16, n_tok, 2 * inter, k) // 4 + 64, dtype=torch.int32,
-                     device=DEV)
-    act = torch.full((n_tok, inter), float("nan"), device=DEV, dtype=torch.bfloat16)
-    ops.linear_swiglu(ops.PackedWeight(ops.interleave_gate_up(wgu)), x, act, n_tok, ws)
-    torch.cuda.synchronize()
-    gu = x.float() @ wgu.float().T
-    want = torch.nn.functional.silu(gu[:, :inter]) * gu[:, inter:]
-    assert not torch.isnan(act.float()).any()
-    assert rel_err(act, want) < 1e-2
-
-
-@pytest.mark.parametrize("n_tok,prefill_len,hq,hkv", [(8, 0, 32, 32), (3, 0, 16, 2), (2 * 96, 96, 8, 2),
-                                                      (1, 0, 8, 8), (2 * 70, 70, 4, 4)])
-def test_linear_rope_kv_fused(n_tok, prefill_len, hq, hkv):
-    hd, page, H = 128, 64, 512
-    b = n_tok // prefill_len if prefill_len else n_tok
-    ctx = (prefill_len or 0) + 40
-    g = torch.Generator(device=DEV).manual_seed(n_tok + hq)
-    w = (torch.randn((hq + 2 * hkv) * hd, H, device=DEV, generator=g) * 0.05).bfloat16()
-    x = torch.randn(n_tok, H, device=DEV, generator=g).bfloat16()
-    kc, vc, bt, _ = _paged_setup(torch.bfloat16, b, hq, hkv, hd, page, ctx)
-    kr, vr = kc.clone(), vc.clone()
-    seq = torch.full((b,), 0 if prefill_len else 37, dtype=torch.int32, device=DEV)
-    q = torch.empty(n_tok, hq * hd, device=DEV, dtype=torch.bfloat16)
-    ws = torch.zeros(ops.linear_workspace(torch.bfloat16, n_tok, w.shape[0], H) // 4 + 64, dtype=torch.int32,
-                     device=DEV)
-    tab = ops.rope_table(256, hd, 10000.0) if prefill_len == 0 else None
-    ops.linear_rope_kv(ops.PackedWeight(w), x, q, kc, vc, bt, seq, n_tok, prefill_len, hq, hkv, 10000.0, ws, tab)
-    qkv = (x.float() @ w.float().T)
-    qr = torch.empty(n_tok, hq * hd, device=DEV)
-    ref.rope_kv_append(qkv, qr, kr, vr, bt, seq, n_tok, prefill_len, hq, hkv, hd, 10000.0)
-    torch.cuda.synchronize()
-    assert rel_err(q, qr) < 1e-2
-    assert rel_err(kc, kr) < 1e-2 and rel_err(vc, vr) < 1e-2
-
-
 def test_linear_bf16_accumulate_and_pitch():
     w = (torch.randn(512, 256, device=DEV) * 0.05).bfloat16()
     x = torch.randn(8, 256, device=DEV).bfloat16()

@@ -3,7 +3,7 @@
 copy of the model).
 
     torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tools/ab_dist.py --tp 2 --layers 40 \
-        --a HX_FUSE_SWIGLU=0 --b HX_FUSE_SWIGLU=1
+        --a HX_AR_PAYLOAD=fp32 --b HX_AR_PAYLOAD=bf16
 
 Environment assignments in --a / --b (comma-separated) are applied while that
 engine is constructed (the engine reads its switches at construction).
