@@ -54,6 +54,9 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     cfg = preset(a.model)
+    n_layers = sum(st.num_layers for st in pipe)
+    if n_layers != cfg.num_layers:   # one stage of a larger pipeline, measured on its own
+        cfg = preset(a.model, num_layers=n_layers)
     eng = Engine(sub, cfg, dtype="bf16", batch=task.batch_size, max_prompt=task.input_len, max_out=task.output_len,
                  comm="dist" if world > 1 else "local", device=dev, weights="device")
     prompt = np.random.default_rng(1).integers(0, cfg.vocab, size=(task.batch_size, task.input_len), dtype=np.int32)
@@ -69,7 +72,8 @@ def main():
                "output_len": task.output_len, "seconds": float(statistics.median(v[:, 0])),
                "prefill_s": float(statistics.median(v[:, 1])), "decode_s": float(statistics.median(v[:, 2])),
                "plan": plan_notation(pipe), "layers": [s.num_layers for s in pipe], "gpus": d,
-               "gpu_type": a.gpu_type, "device_name": torch.cuda.get_device_name(dev)}
+               "gpu_type": a.gpu_type, "device_name": torch.cuda.get_device_name(dev),
+               "model_layers": cfg.num_layers}
         Path(a.out).write_text(json.dumps(doc, indent=1) + "\n")
         print(json.dumps(doc), flush=True)
     if world > 1:
