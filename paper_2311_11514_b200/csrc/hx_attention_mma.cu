@@ -493,9 +493,15 @@ __global__ void __launch_bounds__(AM_THREADS * BPI)
   const int32_t *btb = bt + (size_t)b * max_blocks;
   const int safe = min(nblk, max(0, pos / PAGE - t0 / PAGE));  // blocks not holding the new token
   const uint64_t pol = l2_policy_evict_first();  // each K/V byte is read once per step
+  // this CTA's block-table entries, fetched by many threads at once (one
+  // dependent L2 round trip instead of one per TMA issue of thread 0)
+  constexpr int kMaxBt = 64;  // 64-key blocks per split (contexts up to 4096 tokens per split)
+  __shared__ int bts[kMaxBt];
+  for (int i = threadIdx.x; i < nblk && i < kMaxBt; i += AM_THREADS * BPI) bts[i] = btb[t0 / PAGE + i];
+  __syncthreads();
   auto issue = [&](int i) {
     const int s = i % NS;
-    const int row = (btb[t0 / PAGE + i] * hkv + kvh) * PAGE;
+    const int row = ((i < kMaxBt ? bts[i] : btb[t0 / PAGE + i]) * hkv + kvh) * PAGE;
     uint8_t *kd = ring + s * 2 * BLK, *vd = kd + BLK;
     mbar_arrive_expect_tx(&full[s], 2 * BLK);
     tma_load_2d(kd, &tmk, &full[s], 0, row, pol);
@@ -568,11 +574,25 @@ __global__ void __launch_bounds__(AM_THREADS * BPI)
     const float inv_freq = 1.0f / powf(theta, (float)(2 * i) / 128.0f);
     float sn, cs;
     sincosf((float)pos * inv_freq, &sn, &cs);
-    for (int r = threadIdx.x >> 6; r < 16; r += AM_THREADS * BPI / 64) {
+    constexpr int STEP = AM_THREADS * BPI / 64;   // q rows per pass
+    constexpr int NR = (16 + STEP - 1) / STEP;   // passes
+    __nv_bfloat16 x1r[NR], x2r[NR];
+    const int r0 = threadIdx.x >> 6;
+#pragma unroll
+    for (int k = 0; k < NR; ++k) {  // every load in flight before any is used
+      const int r = r0 + k * STEP;
+      if (r < G) {
+        x1r[k] = row[(kvh * G + r) * HD + i];
+        x2r[k] = row[(kvh * G + r) * HD + i + 64];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < NR; ++k) {
+      const int r = r0 + k * STEP;
+      if (r >= 16) continue;
       float y1 = 0.f, y2 = 0.f;
       if (r < G) {
-        const float x1 = to_f32(row[(kvh * G + r) * HD + i]), x2 = to_f32(row[(kvh * G + r) * HD + i + 64]);
-        const float2 y = rope_rot(x1, x2, cs, sn);
+        const float2 y = rope_rot(to_f32(x1r[k]), to_f32(x2r[k]), cs, sn);
         y1 = y.x;
         y2 = y.y;
       }
@@ -716,15 +736,27 @@ __global__ void __launch_bounds__(AM_THREADS * BPI)
     cluster_sync_all();
     for (int w = split * AM_THREADS * BPI + threadIdx.x; w < G * HD; w += splits * AM_THREADS * BPI) {
       const int r = w / HD, d = w % HD;
+      constexpr int MAXS = 8;  // cluster splits are 2..8
+      float ms[MAXS], ls[MAXS], as[MAXS];
+#pragma unroll
+      for (int c2 = 0; c2 < MAXS; ++c2) {  // all remote loads in flight before any is used
+        if (c2 < splits) {
+          ms[c2] = dsmem_ld_f32(mypart + r * (HD + 2) + HD, c2);
+          ls[c2] = dsmem_ld_f32(mypart + r * (HD + 2) + HD + 1, c2);
+          as[c2] = dsmem_ld_f32(mypart + r * (HD + 2) + d, c2);
+        }
+      }
       float M = -INFINITY;
-      for (int c2 = 0; c2 < splits; ++c2) M = fmaxf(M, dsmem_ld_f32(mypart + r * (HD + 2) + HD, c2));
+#pragma unroll
+      for (int c2 = 0; c2 < MAXS; ++c2)
+        if (c2 < splits) M = fmaxf(M, ms[c2]);
       float L = 0.f, A = 0.f;
-      for (int c2 = 0; c2 < splits; ++c2) {
-        const float ms = dsmem_ld_f32(mypart + r * (HD + 2) + HD, c2);
-        if (ms == -INFINITY) continue;
-        const float cf = exp2f(ms - M);
-        L += dsmem_ld_f32(mypart + r * (HD + 2) + HD + 1, c2) * cf;
-        A += dsmem_ld_f32(mypart + r * (HD + 2) + d, c2) * cf;
+#pragma unroll
+      for (int c2 = 0; c2 < MAXS; ++c2) {
+        if (c2 >= splits || ms[c2] == -INFINITY) continue;
+        const float cf = exp2f(ms[c2] - M);
+        L += ls[c2] * cf;
+        A += as[c2] * cf;
       }
       o[((size_t)b * hq + kvh * G + r) * HD + d] = __float2bfloat16_rn(A / L);
     }
