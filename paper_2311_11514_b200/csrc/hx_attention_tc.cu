@@ -245,6 +245,244 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
+// ------------------------------------------------------------------ persistent variant
+// The one-tile kernel above is latency-bound: 1024 short CTAs (1-4 key blocks
+// at 7B s=512) in ~7 waves, each paying the barrier/TMEM set-up, the first TMA
+// round trip and its drain alone (ncu: 9 % tensor pipe, the top stalls are the
+// mbarrier waits and CTAs waiting to exit). Here one CTA per SM walks the
+// (query tile, head, sequence) items heaviest first (item c, c + G, ...): the
+// producer loads the next item's Q (once the previous item's last S MMA has
+// read the Q buffer: q_empty) and K/V blocks while the current item is still
+// in its softmax / PV / epilogue, and every mbarrier phase is tracked by a
+// global block counter across items. Roles, TMEM map and numerics per item
+// are those of attn_prefill_tc_kernel.
+__global__ void __launch_bounds__(192, 1)
+    attn_prefill_tcp_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmk,
+                            const __grid_constant__ CUtensorMap tmv, const int32_t *bt, __nv_bfloat16 *o, int s_len,
+                            int hq, int hkv, int max_blocks, float sl2, int batch) {
+  extern __shared__ uint8_t smraw[];
+  uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  uint8_t *qs = sm;
+  uint8_t *kv = sm + TC_TILE;
+  uint8_t *ps = sm + 5 * TC_TILE;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(sm + 6 * TC_TILE);
+  uint64_t *q_full = bar, *kv_full = bar + 1, *kv_empty = bar + 3, *s_full = bar + 5, *s_empty = bar + 7,
+           *p_full = bar + 9, *pv_full = bar + 10, *pv_empty = bar + 12, *q_empty = bar + 14;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 15);
+
+  pdl_trigger();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nq = s_len / TC_ROWS;
+  const int per_tile = hq * batch;
+  const int n_items = nq * per_tile;
+  const int G = gridDim.x;
+  // item -> (query tile, head, sequence), heaviest query tiles first
+  auto decode_item = [&](int item, int &qt, int &h, int &b) {
+    qt = nq - 1 - item / per_tile;
+    const int rem = item % per_tile;
+    h = rem % hq;
+    b = rem / hq;
+  };
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tmq);
+    tma_prefetch(&tmk);
+    tma_prefetch(&tmv);
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], 128);
+      mbar_init(&pv_full[i], 1);
+      mbar_init(&pv_empty[i], 128);
+    }
+    mbar_init(p_full, 128);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol = l2_policy_evict_last();
+      pdl_wait();  // q, the K pages and V^T come from the preceding kernels
+      int g = 0, it = 0;
+      for (int item = blockIdx.x; item < n_items; item += G, ++it) {
+        int qt, h, b;
+        decode_item(item, qt, h, b);
+        const int kvh = h / (hq / hkv);
+        if (it > 0) mbar_wait(q_empty, (it - 1) & 1);  // the previous item's S MMAs have read Q
+        mbar_arrive_expect_tx(q_full, TC_TILE);
+        for (int hh = 0; hh < 2; ++hh)
+          tma_load_2d(qs + hh * TC_HALF, &tmq, q_full, h * 128 + hh * 64, b * s_len + qt * TC_ROWS, pol);
+        const int32_t *btb = bt + (size_t)b * max_blocks;
+        for (int j = 0; j <= qt; ++j, ++g) {
+          const int st = g & 1;
+          if (g >= 2) mbar_wait(&kv_empty[st], ((g >> 1) & 1) ^ 1);
+          uint8_t *ks = kv + 2 * st * TC_TILE, *vs = ks + TC_TILE;
+          mbar_arrive_expect_tx(&kv_full[st], 2 * TC_TILE);
+          for (int pg = 0; pg < 2; ++pg) {
+            const int row = (btb[2 * j + pg] * hkv + kvh) * 64;
+            for (int hh = 0; hh < 2; ++hh)
+              tma_load_2d(ks + hh * TC_HALF + pg * 64 * 128, &tmk, &kv_full[st], hh * 64, row, pol);
+          }
+          for (int hh = 0; hh < 2; ++hh)
+            tma_load_2d(vs + hh * TC_HALF, &tmv, &kv_full[st], j * 128 + hh * 64, (b * hkv + kvh) * 128, pol);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(128, 128);
+      auto issue_s = [&](int gs) {
+        const int st = gs & 1;
+        mbar_wait(&kv_full[st], (gs >> 1) & 1);
+        if (gs >= 2) mbar_wait(&s_empty[st], ((gs >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint8_t *ks = kv + 2 * st * TC_TILE;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          umma_bf16(tmem + st * 128, umma_desc_sw128(qs + (kk >> 2) * TC_HALF) + 2 * (kk & 3),
+                    umma_desc_sw128(ks + (kk >> 2) * TC_HALF) + 2 * (kk & 3), idesc, kk > 0 ? 1u : 0u);
+        umma_commit(&s_full[st]);
+      };
+      int g = 0, it = 0;
+      for (int item = blockIdx.x; item < n_items; item += G, ++it) {
+        int qt, h, b;
+        decode_item(item, qt, h, b);
+        const int nblk = qt + 1;
+        mbar_wait(q_full, it & 1);
+        issue_s(g);
+        if (nblk == 1) umma_commit(q_empty);
+        for (int j = 0; j < nblk; ++j) {
+          const int gb = g + j;
+          if (j + 1 < nblk) {
+            issue_s(gb + 1);
+            if (j + 2 == nblk) umma_commit(q_empty);  // the item's last S MMA has been issued
+          }
+          const int st = gb & 1;
+          mbar_wait(p_full, gb & 1);
+          if (gb >= 2) mbar_wait(&pv_empty[st], ((gb >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint8_t *vs = kv + (2 * st + 1) * TC_TILE;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            umma_bf16(tmem + 256 + st * 128, umma_desc_sw128(ps + (kk >> 2) * TC_HALF) + 2 * (kk & 3),
+                      umma_desc_sw128(vs + (kk >> 2) * TC_HALF) + 2 * (kk & 3), idesc, kk > 0 ? 1u : 0u);
+          umma_commit(&pv_full[st]);
+          umma_commit(&kv_empty[st]);
+        }
+        g += nblk;
+      }
+    }
+  } else {
+    const int qq = warp & 3;
+    const int r = qq * 32 + lane;
+    const uint32_t trow = tmem + ((uint32_t)(qq * 32) << 16);
+    int g = 0;
+    for (int item = blockIdx.x; item < n_items; item += G) {
+      int qt, h, b;
+      decode_item(item, qt, h, b);
+      const int nblk = qt + 1;
+      float O[128];
+#pragma unroll
+      for (int c = 0; c < 128; ++c) O[c] = 0.f;
+      float m = -INFINITY, l = 0.f;
+      for (int j = 0; j < nblk; ++j) {
+        const int gb = g + j;
+        const int st = gb & 1;
+        const bool diag = j == qt;
+        mbar_wait(&s_full[st], (gb >> 1) & 1);
+        tc_fence_after();
+        float mx = -INFINITY;
+#pragma unroll
+        for (int c1 = 0; c1 < 128; c1 += 64) {
+          float v[64];
+#pragma unroll
+          for (int c0 = 0; c0 < 64; c0 += 16) tmem_ld16_nw(trow + st * 128 + c1 + c0, v + c0);
+          tmem_wait_ld();
+#pragma unroll
+          for (int k = 0; k < 64; ++k)
+            if (!diag || c1 + k <= r) mx = fmaxf(mx, v[k]);
+        }
+        const float m_new = fmaxf(m, mx * sl2);
+        const float corr = exp2f(m - m_new);
+        if (j > 0) {  // fold PV_{gb-1} into O, rescale to m_new (also frees the P buffer)
+          const int pg = gb - 1;
+          const int pb = pg & 1;
+          mbar_wait(&pv_full[pb], (pg >> 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int c1 = 0; c1 < 128; c1 += 32) {
+            float v[32];
+            tmem_ld16_nw(trow + 256 + pb * 128 + c1, v);
+            tmem_ld16_nw(trow + 256 + pb * 128 + c1 + 16, v + 16);
+            tmem_wait_ld();
+#pragma unroll
+            for (int k = 0; k < 32; ++k) O[c1 + k] = (O[c1 + k] + v[k]) * corr;
+          }
+          tc_fence_before();
+          mbar_arrive(&pv_empty[pb]);
+        }
+        l *= corr;
+#pragma unroll
+        for (int c0 = 0; c0 < 128; c0 += 16) {
+          float v[16];
+          tmem_ld16(trow + st * 128 + c0, v);
+          uint32_t pk[8];
+#pragma unroll
+          for (int k = 0; k < 16; k += 2) {
+            const float p0 = (!diag || c0 + k <= r) ? exp2f(v[k] * sl2 - m_new) : 0.f;
+            const float p1 = (!diag || c0 + k + 1 <= r) ? exp2f(v[k + 1] * sl2 - m_new) : 0.f;
+            l += p0 + p1;
+            pk[k >> 1] = pack_bf16(p0, p1);
+          }
+          *reinterpret_cast<uint4 *>(ps + tc_off(r, c0)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          *reinterpret_cast<uint4 *>(ps + tc_off(r, c0 + 8)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        }
+        tc_fence_before();
+        mbar_arrive(&s_empty[st]);
+        fence_proxy_async_smem();
+        mbar_arrive(p_full);
+        m = m_new;
+      }
+      const int lg = g + nblk - 1;
+      const int pb = lg & 1;
+      mbar_wait(&pv_full[pb], (lg >> 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c0 = 0; c0 < 128; c0 += 16) {
+        float v[16];
+        tmem_ld16(trow + 256 + pb * 128 + c0, v);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) O[c0 + k] += v[k];
+      }
+      tc_fence_before();
+      mbar_arrive(&pv_empty[pb]);  // the last PV buffer is read: the next item may reuse it
+      const float inv = 1.0f / l;
+      __nv_bfloat16 *dst = o + ((size_t)(b * s_len + qt * TC_ROWS + r) * hq + h) * 128;
+#pragma unroll
+      for (int c0 = 0; c0 < 128; c0 += 8) {
+        uint4 u;
+        u.x = pack_bf16(O[c0] * inv, O[c0 + 1] * inv);
+        u.y = pack_bf16(O[c0 + 2] * inv, O[c0 + 3] * inv);
+        u.z = pack_bf16(O[c0 + 4] * inv, O[c0 + 5] * inv);
+        u.w = pack_bf16(O[c0 + 6] * inv, O[c0 + 7] * inv);
+        *reinterpret_cast<uint4 *>(dst + c0) = u;
+      }
+      g += nblk;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
 // vt[((b * hkv + h) * 128 + d) * s + i] = v of token (b, i), kv head h, dim d,
 // read from the packed qkv rows; 64 x 64 tiles through smem with 4-byte
 // (bf16 pair) accesses on both sides
@@ -298,12 +536,26 @@ extern "C" int hx_attn_prefill_tc(const void *q, const void *k_cache, const void
   if (!rc) rc = make_tma_bf16_sw128(&mv, vt, (long)batch * hkv * 128, s_len, s_len, 128);
   if (rc) return rc;
   const size_t smem = 1024 + 6 * TC_TILE + 16 * 8 + 16;
+  const float sl2 = 1.4426950408889634f / sqrtf(128.f);
+  static const bool persistent = [] {  // HX_PREFILL_TC_P=0: one CTA per (query tile, head, sequence)
+    const char *e = getenv("HX_PREFILL_TC_P");
+    return e ? atoi(e) != 0 : true;
+  }();
+  if (persistent) {
+    static bool attrp = false;
+    if (!attrp) {
+      cudaFuncSetAttribute(attn_prefill_tcp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attrp = true;
+    }
+    const int items = (s_len / 128) * hq * batch;
+    return launch(attn_prefill_tcp_kernel, dim3(items < 148 ? items : 148), dim3(192), smem, as_stream(stream), mq, mk,
+                  mv, block_table, (__nv_bfloat16 *)o, s_len, hq, hkv, max_blocks, sl2, batch);
+  }
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(attn_prefill_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  const float sl2 = 1.4426950408889634f / sqrtf(128.f);
   return launch(attn_prefill_tc_kernel, dim3(s_len / 128, hq, batch), dim3(192), smem, as_stream(stream), mq, mk, mv,
                 block_table, (__nv_bfloat16 *)o, s_len, hq, hkv, max_blocks, sl2);
 }
