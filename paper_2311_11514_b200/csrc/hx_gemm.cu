@@ -1108,15 +1108,19 @@ extern "C" int hx_linear(const void *w, const void *x, void *y, int dtype, int y
     p.counters = reinterpret_cast<int *>(workspace);
     p.ws = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(workspace) + kTicketBytes);
   }
-  static const bool persistent = [] {  // HX_GEMM_PERSISTENT=0: one CTA per tile (round-1 kernel)
+  static const int persistent = [] {  // 0: one CTA per tile (round-1 kernel); 2: every shape <= 4096 tiles
     const char *e = getenv("HX_GEMM_PERSISTENT");
-    return e ? atoi(e) != 0 : true;
+    return e ? atoi(e) : 1;
   }();
-  // measured: +4-10 % at the engine's prefill shapes (<= 4096 token rows; 7B / 13B
-  // prompts, 70B micro-batches of 2048 rows, up to ~3600 tiles), but -10-20 % on
-  // one-shot 32768-row GEMMs (>= 8192 tiles): there the per-tile kernel is kept
+  // measured in the engine (same-box A/B, profiles/r02/prefill_gemm_persistent.txt):
+  // 7B one-shot prefill (4096 token rows) 54.2 -> 51.9 ms persistent; C3 asym
+  // (2048-row micro-batches, <= 1024 tiles) 67.0 -> 64.5 ms; but 70B [1,1]
+  // micro-batched gate/up (2048 x 57344, 3584 tiles) costs 2415 -> 2529 ms when
+  // persistent, and one-shot 32768-row GEMMs (>= 8192 tiles) lose 10-20 %. So:
+  // persistent up to 1024 tiles, and for >= 4096-row GEMMs up to 4096 tiles.
   const int n_tiles = ((p.M + BM - 1) / BM) * ((p.N + 255) / 256);
-  if (persistent && pl.bn == 256 && pl.splits == 1 && !p.a_is_weight && n_tiles <= 4096) {
+  if (persistent && pl.bn == 256 && pl.splits == 1 && !p.a_is_weight && n_tiles <= 4096 &&
+      (n_tiles <= 1024 || p.M >= 4096 || persistent == 2)) {
     constexpr int STG = 4;
     const size_t smem = 1024 + STG * (BM * BK * 2 + 256 * BK * 2) + (2 * STG + 4) * 8 + 16;
     static bool attr_done = false;
