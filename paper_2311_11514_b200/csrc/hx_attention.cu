@@ -390,6 +390,9 @@ static int tma_decode_splits(int batch, int hkv, int max_ctx, int *ns) {
   if (env_ns == 6) {
     n = 6;
     s = 148 / pairs;
+  } else if (env_ns == 2) {  // 2-deep ring, ~71 KB: 3 CTAs per SM
+    n = 2;
+    s = 3 * 148 / pairs;
   } else {
     n = 3;
     s = decode_splits(batch, hkv, max_ctx);

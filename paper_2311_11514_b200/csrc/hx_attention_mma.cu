@@ -394,6 +394,12 @@ __global__ void __launch_bounds__(AM_THREADS)
 // 64-column 128B-swizzled boxes for K, two for V) into a DEC_NS-deep mbarrier
 // ring: 4 instructions per block instead of 2048 cp.async, so the warps only
 // issue ldmatrix / mma / softmax. ldmatrix addresses apply the same XOR swizzle.
+unsigned long long *hx_trace_slots(size_t n);  // hx_gemm.cu (hx_debug_trace)
+__device__ __forceinline__ unsigned long long attn_globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ uint32_t sw128_addr(uint32_t base, int r, int col) {
   const int half = col >> 6, chunk = (col & 63) >> 3;
   return base + half * 8192 + r * 128 + ((chunk ^ (r & 7)) << 4) + ((col & 7) << 1);
@@ -403,53 +409,42 @@ __device__ __forceinline__ uint32_t sw128_addr(uint32_t base, int r, int col) {
 // (HX_LINEAR_DEFER_REDUCE, fp32 output `q` with row pitch ldq): its split tiles
 // are summed here from the GEMM's partial slots, in CTA order, and rounded to
 // bf16 -- the bits the GEMM's own fix-up would have stored -- so the GEMM ends
-// without its serial fix-up tail. Up to 4 (row, pair) items per thread have
-// their partial loads in flight together.
-template <int G>
-__device__ __forceinline__ void gather_qkv_pairs(const SKView &v, const float *y, long ldy, int b, const int *n,
-                                                 int cnt, float2 *out) {
-  constexpr int NI = 4, MAXC = 8;
-  SkTile ti[NI];
-#pragma unroll
-  for (int j = 0; j < NI; ++j) {
-    out[j] = make_float2(0.f, 0.f);
-    ti[j] = SkTile{0, -1, true};
-    if (j < cnt) {
-      ti[j] = sk_tile(v, n[j] / kSkRows);
-      if (ti[j].whole) out[j] = make_float2(y[(long)b * ldy + n[j]], y[(long)b * ldy + n[j] + 64]);
-    }
-  }
-  for (int base = 0;; base += MAXC) {
-    float2 f[NI][MAXC];
-    bool more = false;
-#pragma unroll
-    for (int j = 0; j < NI; ++j)
-#pragma unroll
-      for (int k = 0; k < MAXC; ++k) {
-        const int cc = j < cnt && !ti[j].whole ? ti[j].c_first + base + k : INT_MAX;
-        if (cc <= ti[j].c_last) {
-          const int tt = n[j] / kSkRows;
-          const int sl = 2 * cc + (sk_start(cc, v.units, v.G) < tt * v.KB ? 1 : 0);
-          const float *src = v.ws + ((size_t)sl * v.BN + b) * kSkRows + n[j] % kSkRows;
-          f[j][k] = make_float2(__ldcg(src), __ldcg(src + 64));
-        }
-      }
-#pragma unroll
-    for (int j = 0; j < NI; ++j) {
-      if (j >= cnt || ti[j].whole) continue;
+// without its serial fix-up tail. A head is one 128-row tile; its contributor
+// range (tl) is computed once per CTA before the dependency wait. A thread
+// gathers features i0..i0+3 and i0+64..i0+67 of one head (a RoPE rotate-half
+// quad pair) with 16-byte loads, every contributor's loads in flight together.
+__device__ __forceinline__ void gather_quad_pair(const SKView &v, const float *y, long ldy, int b, int head, int i0,
+                                                 const SkTile &ti, float (&lo)[4], float (&hi)[4]) {
+  float4 l = make_float4(0.f, 0.f, 0.f, 0.f), h = l;
+  if (ti.whole()) {
+    const float *src = y + (long)b * ldy + head * kSkRows + i0;
+    l = *reinterpret_cast<const float4 *>(src);
+    h = *reinterpret_cast<const float4 *>(src + 64);
+  } else {
+    constexpr int MAXC = 10;
+    for (int cb = ti.c_first; cb <= ti.c_last; cb += MAXC) {
+      float4 fl[MAXC], fh[MAXC];
 #pragma unroll
       for (int k = 0; k < MAXC; ++k)
-        if (ti[j].c_first + base + k <= ti[j].c_last) {
-          out[j].x += f[j][k].x;
-          out[j].y += f[j][k].y;
+        if (cb + k <= ti.c_last) {
+          const float *src = v.ws + ((size_t)ti.slot(cb + k) * v.BN + b) * kSkRows + i0;
+          fl[k] = __ldcg(reinterpret_cast<const float4 *>(src));
+          fh[k] = __ldcg(reinterpret_cast<const float4 *>(src + 64));
         }
-      more |= ti[j].c_first + base + MAXC <= ti[j].c_last;
-    }
-    if (!more) break;
-  }
 #pragma unroll
-  for (int j = 0; j < NI; ++j)  // the bf16 value the GEMM would have stored
-    out[j] = make_float2(__bfloat162float(__float2bfloat16_rn(out[j].x)), __bfloat162float(__float2bfloat16_rn(out[j].y)));
+      for (int k = 0; k < MAXC; ++k)
+        if (cb + k <= ti.c_last) {
+          l.x += fl[k].x; l.y += fl[k].y; l.z += fl[k].z; l.w += fl[k].w;
+          h.x += fh[k].x; h.y += fh[k].y; h.z += fh[k].z; h.w += fh[k].w;
+        }
+    }
+  }
+  const float lv[4] = {l.x, l.y, l.z, l.w}, hv[4] = {h.x, h.y, h.z, h.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {  // the bf16 value the GEMM would have stored
+    lo[j] = __bfloat162float(__float2bfloat16_rn(lv[j]));
+    hi[j] = __bfloat162float(__float2bfloat16_rn(hv[j]));
+  }
 }
 
 template <int G, bool ROPE, int NS, int BPI, bool CL, bool DEF = false>
@@ -457,7 +452,7 @@ __global__ void __launch_bounds__(AM_THREADS * BPI)
     attn_decode_tma_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
                            const __nv_bfloat16 *q, const int32_t *bt, const int32_t *seq_lens, __nv_bfloat16 *o,
                            int hkv, int max_blocks, float sl2, float *ws, int *counters, __nv_bfloat16 *kc,
-                           __nv_bfloat16 *vc, float theta, SKView skv, long ldq) {
+                           __nv_bfloat16 *vc, float theta, SKView skv, long ldq, unsigned long long *trace, int prewait) {
   constexpr int HD = 128, LD = HD + 8, PAGE = 64;
   constexpr uint32_t BLK = PAGE * HD * 2;  // 16 KB per tensor per block
   extern __shared__ __align__(1024) uint8_t smraw[];
@@ -469,6 +464,12 @@ __global__ void __launch_bounds__(AM_THREADS * BPI)
   float *mypart = red + 4 * BPI * 16 * (HD + 2);  // [G][HD + 2] this split's combined partial (CL)
   __shared__ int s_last;
   pdl_trigger();
+  // hx_debug_trace: start, wait done, end, smid | 1 << 40, q ready, loop done, partials combined, nblk
+  unsigned long long *tr = trace ? trace + 8 * (blockIdx.x + (size_t)blockIdx.y * gridDim.x) : nullptr;
+  auto stamp = [&](int f) {
+    if (tr && threadIdx.x == 0) tr[f] = attn_globaltimer();
+  };
+  stamp(0);
   // CL: the splits of one (batch, kv-head) pair form a thread-block cluster and
   // combine through DSMEM; otherwise grid.y = splits and the last split to
   // finish (ticket) combines through the workspace
@@ -498,6 +499,29 @@ __global__ void __launch_bounds__(AM_THREADS * BPI)
   constexpr int kMaxBt = 64;  // 64-key blocks per split (contexts up to 4096 tokens per split)
   __shared__ int bts[kMaxBt];
   for (int i = threadIdx.x; i < nblk && i < kMaxBt; i += AM_THREADS * BPI) bts[i] = btb[t0 / PAGE + i];
+  // DEF: the contributor ranges of this pair's G q heads, its k head and v head
+  // (GEMM geometry only -- independent of the producer's data)
+  __shared__ SkTile s_tiles[DEF ? G + 2 : 1];
+  if constexpr (DEF) {
+    if (threadIdx.x < G + 2) {
+      const int h = threadIdx.x < G ? kvh * G + threadIdx.x : hq + (threadIdx.x == G ? 0 : hkv) + kvh;
+      s_tiles[threadIdx.x] = sk_tile(skv, h);
+    }
+  }
+  // RoPE angles of the new position (pos is known before the wait): feature
+  // threadIdx % 64 (ROPE), features 4 (threadIdx % 16) + 0..3 (DEF)
+  float rope_sn = 0.f, rope_cs = 0.f;
+  float qsn[4], qcs[4];
+  if constexpr (DEF) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float inv_freq = 1.0f / powf(theta, (float)(2 * (4 * (threadIdx.x & 15) + j)) / 128.0f);
+      sincosf((float)pos * inv_freq, &qsn[j], &qcs[j]);
+    }
+  } else if constexpr (ROPE) {
+    const float inv_freq = 1.0f / powf(theta, (float)(2 * (threadIdx.x & 63)) / 128.0f);
+    sincosf((float)pos * inv_freq, &rope_sn, &rope_cs);
+  }
   __syncthreads();
   auto issue = [&](int i) {
     const int s = i % NS;
@@ -509,7 +533,7 @@ __global__ void __launch_bounds__(AM_THREADS * BPI)
     tma_load_2d(vd, &tmv, &full[s], 0, row, pol);
     tma_load_2d(vd + BLK / 2, &tmv, &full[s], 64, row, pol);
   };
-  const int pre = min(NS, safe);
+  const int pre = min(min(NS, prewait), safe);
   if (threadIdx.x == 0) {
     tma_prefetch(&tmk);
     tma_prefetch(&tmv);
@@ -518,50 +542,45 @@ __global__ void __launch_bounds__(AM_THREADS * BPI)
     for (int i = 0; i < pre; ++i) issue(i);
   }
   pdl_wait();
+  stamp(1);
+  if (tr && threadIdx.x == 0) {
+    unsigned sm;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(sm));
+    tr[3] = sm | (1ull << 40);
+    tr[7] = (unsigned long long)nblk | ((unsigned long long)split << 16);
+    tr[2] = 0;
+  }
   if constexpr (DEF) {
     static_assert(ROPE, "the deferred QKV path is the fused RoPE + KV-append path");
-    const int i = threadIdx.x & 63;
     const float *y = reinterpret_cast<const float *>(q);
-    const float inv_freq = 1.0f / powf(theta, (float)(2 * i) / 128.0f);
-    float sn, cs;
-    sincosf((float)pos * inv_freq, &sn, &cs);
-    constexpr int STEP = AM_THREADS * BPI / 64;  // q rows handled per pass
-    for (int r0 = threadIdx.x >> 6; r0 < 16; r0 += 4 * STEP) {
-      int n[4], cnt = 0;
+    const int i0 = 4 * (threadIdx.x & 15);
+    for (int e = threadIdx.x; e < (16 - G) * (HD / 8); e += AM_THREADS * BPI)  // zero padding rows G..15
+      *reinterpret_cast<uint4 *>(qs + (G + e / (HD / 8)) * LD + (e % (HD / 8)) * 8) = make_uint4(0, 0, 0, 0);
+    for (int r = threadIdx.x >> 4; r < G; r += AM_THREADS * BPI / 16) {
+      float lo[4], hi[4];
+      gather_quad_pair(skv, y, ldq, b, kvh * G + r, i0, s_tiles[r], lo, hi);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const int r = r0 + j * STEP;
-        if (r < G) n[cnt++] = (kvh * G + r) * HD + i;
-      }
-      float2 xv[4];
-      gather_qkv_pairs<G>(skv, y, ldq, b, n, cnt, xv);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int r = r0 + j * STEP;
-        if (r >= 16) continue;
-        float y1 = 0.f, y2 = 0.f;
-        if (r < G) {
-          const float2 yy = rope_rot(xv[j].x, xv[j].y, cs, sn);
-          y1 = yy.x;
-          y2 = yy.y;
-        }
-        qs[r * LD + i] = __float2bfloat16_rn(y1);
-        qs[r * LD + i + 64] = __float2bfloat16_rn(y2);
+        const float2 yy = rope_rot(lo[j], hi[j], qcs[j], qsn[j]);
+        qs[r * LD + i0 + j] = __float2bfloat16_rn(yy.x);
+        qs[r * LD + i0 + 64 + j] = __float2bfloat16_rn(yy.y);
       }
     }
-    if (t0 <= pos && pos < t1) {
+    if (t0 <= pos && pos < t1 && threadIdx.x < 32) {  // threads 0-15: the new k, 16-31: the new v
       const size_t slot = (((size_t)btb[pos / PAGE] * hkv + kvh) * PAGE + pos % PAGE) * HD;
-      const bool is_k = threadIdx.x < 64;
-      int n[1] = {((is_k ? hq : hq + hkv) + kvh) * HD + i};
-      float2 xv[4];
-      gather_qkv_pairs<G>(skv, y, ldq, b, n, threadIdx.x < 128 ? 1 : 0, xv);
-      if (is_k) {
-        const float2 yy = rope_rot(xv[0].x, xv[0].y, cs, sn);
-        kc[slot + i] = __float2bfloat16_rn(yy.x);
-        kc[slot + i + 64] = __float2bfloat16_rn(yy.y);
-      } else if (threadIdx.x < 128) {
-        vc[slot + i] = __float2bfloat16_rn(xv[0].x);
-        vc[slot + i + 64] = __float2bfloat16_rn(xv[0].y);
+      const bool is_k = threadIdx.x < 16;
+      float lo[4], hi[4];
+      gather_quad_pair(skv, y, ldq, b, (is_k ? hq : hq + hkv) + kvh, i0, s_tiles[is_k ? G : G + 1], lo, hi);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (is_k) {
+          const float2 yy = rope_rot(lo[j], hi[j], qcs[j], qsn[j]);
+          kc[slot + i0 + j] = __float2bfloat16_rn(yy.x);
+          kc[slot + i0 + 64 + j] = __float2bfloat16_rn(yy.y);
+        } else {
+          vc[slot + i0 + j] = __float2bfloat16_rn(lo[j]);
+          vc[slot + i0 + 64 + j] = __float2bfloat16_rn(hi[j]);
+        }
       }
       fence_proxy_async_global();  // the page is about to be read back by TMA
     }
@@ -571,9 +590,7 @@ __global__ void __launch_bounds__(AM_THREADS * BPI)
     // range holds the new token also rotates its k and appends k, v to the page
     const int i = threadIdx.x & 63;
     const __nv_bfloat16 *row = q + (size_t)b * (hq + 2 * hkv) * HD;
-    const float inv_freq = 1.0f / powf(theta, (float)(2 * i) / 128.0f);
-    float sn, cs;
-    sincosf((float)pos * inv_freq, &sn, &cs);
+    const float sn = rope_sn, cs = rope_cs;
     constexpr int STEP = AM_THREADS * BPI / 64;   // q rows per pass
     constexpr int NR = (16 + STEP - 1) / STEP;   // passes
     __nv_bfloat16 x1r[NR], x2r[NR];
@@ -621,6 +638,7 @@ __global__ void __launch_bounds__(AM_THREADS * BPI)
     }
   }
   __syncthreads();
+  stamp(4);
   int issued = pre;  // meaningful in thread 0 only
   if (threadIdx.x == 0)
     for (; issued < NS && issued < nblk; ++issued) issue(issued);
@@ -686,6 +704,7 @@ __global__ void __launch_bounds__(AM_THREADS * BPI)
     }
   }
   __syncthreads();  // ring no longer read: `red` may overwrite it
+  stamp(5);
 #pragma unroll
   for (int hh = 0; hh < 2; ++hh) {
     l[hh] += __shfl_xor_sync(0xffffffffu, l[hh], 1);
@@ -729,11 +748,15 @@ __global__ void __launch_bounds__(AM_THREADS * BPI)
       if (d == 0) { part[HD] = M; part[HD + 1] = L; }
     }
   }
-  if (splits == 1) return;
+  if (splits == 1) {
+    stamp(2);
+    return;
+  }
   if constexpr (CL) {
     // every split's (A, M, L) sits in its own smem: combine across the cluster
     // over DSMEM, each CTA producing an interleaved 1/splits of the outputs
     cluster_sync_all();
+    stamp(6);
     for (int w = split * AM_THREADS * BPI + threadIdx.x; w < G * HD; w += splits * AM_THREADS * BPI) {
       const int r = w / HD, d = w % HD;
       constexpr int MAXS = 8;  // cluster splits are 2..8
@@ -761,6 +784,7 @@ __global__ void __launch_bounds__(AM_THREADS * BPI)
       o[((size_t)b * hq + kvh * G + r) * HD + d] = __float2bfloat16_rn(A / L);
     }
     cluster_sync_all();  // peers have read this CTA's partial before it exits
+    stamp(2);
     return;
   }
   __syncthreads();
@@ -828,12 +852,18 @@ static int launch_decode_tma_g(dim3 grid, const CUtensorMap &mk, const CUtensorM
     attr = true;
   }
   const float sl2 = 1.4426950408889634f / sqrtf(128.f);
+  unsigned long long *tr = hx_trace_slots((size_t)grid.x * grid.y);
+  static const int prewait = [] {  // KV blocks streamed before the dependency wait (HX_ATTN_PREWAIT, tuning)
+    const char *e = getenv("HX_ATTN_PREWAIT");
+    return e ? atoi(e) : NS;
+  }();
   if constexpr (CL)
     return launch_cluster(kern, dim3(grid.x * grid.y), dim3(AM_THREADS * BPI), smem, st, (int)grid.y, mk, mv,
                           (const __nv_bfloat16 *)q, bt, sl, (__nv_bfloat16 *)o, hkv, maxb, sl2, ws, cnt,
-                          (__nv_bfloat16 *)kc, (__nv_bfloat16 *)vc, theta, skv, ldq);
+                          (__nv_bfloat16 *)kc, (__nv_bfloat16 *)vc, theta, skv, ldq, tr, prewait);
   return launch(kern, grid, dim3(AM_THREADS * BPI), smem, st, mk, mv, (const __nv_bfloat16 *)q, bt, sl,
-                (__nv_bfloat16 *)o, hkv, maxb, sl2, ws, cnt, (__nv_bfloat16 *)kc, (__nv_bfloat16 *)vc, theta, skv, ldq);
+                (__nv_bfloat16 *)o, hkv, maxb, sl2, ws, cnt, (__nv_bfloat16 *)kc, (__nv_bfloat16 *)vc, theta, skv, ldq,
+                tr, prewait);
 }
 
 static const int g_attn_cluster = [] {  // split-KV combine over DSMEM clusters (HX_ATTN_CLUSTER=0: workspace)
@@ -857,6 +887,12 @@ int launch_decode_tma(int G, dim3 grid, const void *q, const void *kc, const voi
   if (skv) {  // deferred QKV (fused RoPE + KV append), 3-deep ring, 1 block per iteration
     if (!rope || ns == 6) return HX_ERR_UNSUPPORTED;
 #define HX_TMA_DEF(GG)                                                                                              \
+  if (ns == 2)                                                                                                     \
+    return grid.y >= 2 && grid.y <= 8                                                                              \
+               ? launch_decode_tma_g<GG, true, 2, 1, true, true>(grid, mk, mv, q, bt, sl, o, hkv, maxb, ws, cnt, k, v, \
+                                                                 theta, st, *skv, ldq)                             \
+               : launch_decode_tma_g<GG, true, 2, 1, false, true>(grid, mk, mv, q, bt, sl, o, hkv, maxb, ws, cnt, k,  \
+                                                                  v, theta, st, *skv, ldq);                        \
   if (grid.y >= 2 && grid.y <= 8 && g_attn_cluster)                                                               \
     return launch_decode_tma_g<GG, true, 3, 1, true, true>(grid, mk, mv, q, bt, sl, o, hkv, maxb, ws, cnt, k, v, theta, \
                                                            st, *skv, ldq);                                          \
@@ -873,6 +909,10 @@ int launch_decode_tma(int G, dim3 grid, const void *q, const void *kc, const voi
     return HX_ERR_UNSUPPORTED;
   }
 #define HX_TMA_G(GG)                                                                                               \
+  if (ns == 2 && rope)                                                                                             \
+    return grid.y >= 2 && grid.y <= 8                                                                              \
+               ? launch_decode_tma_g<GG, true, 2, 1, true>(grid, mk, mv, q, bt, sl, o, hkv, maxb, ws, cnt, k, v, theta, st) \
+               : launch_decode_tma_g<GG, true, 2, 1>(grid, mk, mv, q, bt, sl, o, hkv, maxb, ws, cnt, k, v, theta, st);      \
   if (ns == 6)                                                                                                     \
     return rope ? launch_decode_tma_g<GG, true, 6, 2>(grid, mk, mv, q, bt, sl, o, hkv, maxb, ws, cnt, k, v, theta, st) \
                 : launch_decode_tma_g<GG, false, 6, 2>(grid, mk, mv, q, bt, sl, o, hkv, maxb, ws, cnt, k, v, theta, st); \

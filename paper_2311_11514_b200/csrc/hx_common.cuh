@@ -380,12 +380,10 @@ constexpr int kSkRows = 128;
 
 __device__ __forceinline__ int sk_start(int c, int units, int G) { return (int)((unsigned)(c * units) / (unsigned)G); }
 
-// first CTA whose range contains unit u
+// first CTA whose range contains unit u: the largest c with sk_start(c) <= u,
+// i.e. c * units < (u + 1) * G (one division; every CTA owns >= 1 unit)
 __device__ __forceinline__ int sk_owner(int u, int units, int G) {
-  int c = (int)((unsigned)(u * G) / (unsigned)units);
-  while (c + 1 < G && sk_start(c + 1, units, G) <= u) ++c;
-  while (c > 0 && sk_start(c, units, G) > u) --c;
-  return c;
+  return min(G - 1, (int)(((unsigned)(u + 1) * (unsigned)G - 1u) / (unsigned)units));
 }
 
 struct SKView {
@@ -396,24 +394,29 @@ struct SKView {
 // host: the view of hx_linear(n_tok, n_out, k_dim) deferred into `workspace`
 int sk_view_for(int n_tok, int n_out, int k_dim, const void *workspace, SKView *v);
 
+// tile tt of a deferred GEMM: CTAs c_first..c_last contributed; c_first's
+// partial sits in slot0 (2 c_first, or 2 c_first + 1 when the tile is the last
+// segment of a range that began before it), every later contributor began
+// inside the tile (its first segment, slot 2 c); one contributor = a whole tile
+// stored straight to y
 struct SkTile {
-  int c_first, c_last;
-  bool whole;
+  int c_first, c_last, slot0;
+  __device__ __forceinline__ bool whole() const { return c_first == c_last; }
+  __device__ __forceinline__ int slot(int c) const { return c == c_first ? slot0 : 2 * c; }
 };
 
 __device__ __forceinline__ SkTile sk_tile(const SKView &v, int tt) {
   SkTile t;
   t.c_first = sk_owner(tt * v.KB, v.units, v.G);
   t.c_last = sk_owner((tt + 1) * v.KB - 1, v.units, v.G);
-  t.whole = t.c_first == t.c_last && sk_start(t.c_first, v.units, v.G) <= tt * v.KB &&
-            (t.c_first + 1 >= v.G ? v.units : sk_start(t.c_first + 1, v.units, v.G)) >= (tt + 1) * v.KB;
+  t.slot0 = 2 * t.c_first + (sk_start(t.c_first, v.units, v.G) < tt * v.KB ? 1 : 0);
   return t;
 }
 
 __device__ __forceinline__ float4 sk_gather4(const SKView &v, const float *y, long ldy, int t, int n) {
   const int tt = n / kSkRows, r = n % kSkRows;
   const SkTile ti = sk_tile(v, tt);
-  if (ti.whole) return *reinterpret_cast<const float4 *>(y + (long)t * ldy + n);
+  if (ti.whole()) return *reinterpret_cast<const float4 *>(y + (long)t * ldy + n);
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   constexpr int MAXC = 8;  // all contributors' loads in flight together
   for (int cb = ti.c_first; cb <= ti.c_last; cb += MAXC) {
@@ -421,44 +424,13 @@ __device__ __forceinline__ float4 sk_gather4(const SKView &v, const float *y, lo
 #pragma unroll
     for (int i = 0; i < MAXC; ++i) {
       const int cc = cb + i;
-      if (cc <= ti.c_last) {
-        const int sl = 2 * cc + (sk_start(cc, v.units, v.G) < tt * v.KB ? 1 : 0);
-        f[i] = __ldcg(reinterpret_cast<const float4 *>(v.ws + ((size_t)sl * v.BN + t) * kSkRows + r));
-      }
+      if (cc <= ti.c_last)
+        f[i] = __ldcg(reinterpret_cast<const float4 *>(v.ws + ((size_t)ti.slot(cc) * v.BN + t) * kSkRows + r));
     }
 #pragma unroll
     for (int i = 0; i < MAXC; ++i) {
       if (cb + i <= ti.c_last) {
         acc.x += f[i].x; acc.y += f[i].y; acc.z += f[i].z; acc.w += f[i].w;
-      }
-    }
-  }
-  return acc;
-}
-
-// features n and n + 64 of token t (one 128-row tile: a RoPE rotate-half pair)
-__device__ __forceinline__ float2 sk_gather_pair(const SKView &v, const float *y, long ldy, int t, int n) {
-  const int tt = n / kSkRows, r = n % kSkRows;
-  const SkTile ti = sk_tile(v, tt);
-  if (ti.whole) return make_float2(y[(long)t * ldy + n], y[(long)t * ldy + n + 64]);
-  float2 acc = make_float2(0.f, 0.f);
-  constexpr int MAXC = 8;
-  for (int cb = ti.c_first; cb <= ti.c_last; cb += MAXC) {
-    float2 f[MAXC];
-#pragma unroll
-    for (int i = 0; i < MAXC; ++i) {
-      const int cc = cb + i;
-      if (cc <= ti.c_last) {
-        const int sl = 2 * cc + (sk_start(cc, v.units, v.G) < tt * v.KB ? 1 : 0);
-        const float *src = v.ws + ((size_t)sl * v.BN + t) * kSkRows + r;
-        f[i] = make_float2(__ldcg(src), __ldcg(src + 64));
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < MAXC; ++i) {
-      if (cb + i <= ti.c_last) {
-        acc.x += f[i].x;
-        acc.y += f[i].y;
       }
     }
   }

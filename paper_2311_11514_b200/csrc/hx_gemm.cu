@@ -615,8 +615,8 @@ __global__ void __launch_bounds__(192, 2)
             for (int i = 0; i < MAXC; ++i) {
               const int cc = cb + i;
               if (cc <= c_last) {
-                // tile t is the first segment of cc unless cc started before the tile
-                const int sl = 2 * cc + (sk_start(cc, p.units, G) < t * p.KB ? 1 : 0);
+                // tile t is the first segment of cc unless cc started before the tile (c_first only)
+                const int sl = 2 * cc + (cc == c_first && sk_start(cc, p.units, G) < t * p.KB ? 1 : 0);
                 const float *src = p.ws + (size_t)sl * BM * BN + (size_t)ch * BM + row;
 #pragma unroll
                 for (int j = 0; j < 16; ++j) f[i][j] = __ldcg(src + (size_t)j * BM);
@@ -929,6 +929,17 @@ static int sk_grid(int units) { return std::min(units, sk_ctas()); }
 // seg0 accumulator ready, seg0 epilogue done, last-seg accumulator ready, #segments)
 static unsigned long long *g_trace = nullptr;
 static size_t g_trace_cap = 0, g_trace_pos = 0;
+
+// n CTA slots of the same trace for another traced kernel (decode attention), or null
+namespace hx {
+unsigned long long *hx_trace_slots(size_t n);
+}
+unsigned long long *hx::hx_trace_slots(size_t n) {
+  if (!g_trace || g_trace_pos + n > g_trace_cap) return nullptr;
+  unsigned long long *t = g_trace + 8 * g_trace_pos;
+  g_trace_pos += n;
+  return t;
+}
 
 extern "C" size_t hx_linear_workspace(int dtype, int n_tok, int n_out, int k_dim) {
   if (dtype != HX_BF16) return 0;

@@ -48,6 +48,8 @@ seq.append((e.w["lm_head"], e.hl, e.logits))
 lib.hx_debug_trace(buf.data_ptr(), cap)
 if full:
     eng._reset(b, s_in, 4)
+    for ex in eng.execs:  # decode at context s_in (the prompt's pages), not an empty cache
+        ex.kv.seq_lens.fill_(s_in)
 g = torch.cuda.CUDAGraph()
 with torch.cuda.graph(g):
     if full:
@@ -84,6 +86,11 @@ for k, name in enumerate(names):
           f"wait-after-prev {sel[:, 2].mean():6.2f}  tail {sel[:, 3].mean():6.2f}  run-after-wait {sel[:, 4].mean():6.2f}")
 total = (tr[:, 2].max() - tr[:, 0].min()) / 1e3
 print(f"total wall of the traced GEMM sequence: {total:.1f} us over {n} launches")
+# launch lead: previous GEMM's last CTA end - this GEMM's first CTA start (> 0: resident before it ended)
+lead = [(tr[(i - 1) * G:i * G, 2].max() - tr[i * G:(i + 1) * G, 0].min()) / 1e3 for i in range(1, n)]
+for k, name in enumerate(names):
+    sel = lead[(k - 1) % 4::4]
+    print(f"launch lead {name:6s}: mean {np.mean(sel):6.2f} us  min {np.min(sel):6.2f}  max {np.max(sel):6.2f}")
 
 if "--detail" in sys.argv:
     for idx in (5, 6, 7):
