@@ -161,6 +161,15 @@ int hx_tp_allreduce_push_residual_rmsnorm_ex(float *x, const float *own_part, vo
                                              int tp, int max_tok, int *state, const float *gain, void *out,
                                              int out_dtype, int n_tok, int hidden, float eps, int payload_dtype,
                                              hx_stream_t stream);
+/* The same after a deferred row-parallel GEMM (hx_linear with
+ * HX_LINEAR_DEFER_REDUCE into own_part, workspace gemm_workspace, reduction
+ * dim k_dim): the GEMM's split tiles are summed from its partial slots in CTA
+ * order while the row is read (bitwise the fix-up's result), so the O / down
+ * GEMM ends without its split-K fix-up tail. push mode only. */
+int hx_tp_allreduce_push_residual_rmsnorm_sk(float *x, const float *own_part, const void *gemm_workspace, int k_dim,
+                                             void *const *inboxes, int rank, int tp, int max_tok, int *state,
+                                             const float *gain, void *out, int out_dtype, int n_tok, int hidden,
+                                             float eps, int payload_dtype, hx_stream_t stream);
 
 /* ---- Inter-stage reshard over NVLink P2P (decode hand-off and token return).
  * Replaces the leader send + broadcast of PAPER.md:197 (modelled by

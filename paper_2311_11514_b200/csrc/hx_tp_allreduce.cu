@@ -198,7 +198,7 @@ struct ArPayload<__nv_bfloat16> {
 template <typename TO, typename PL>
 __global__ void __launch_bounds__(256)
     tp_ar_push_rmsnorm_kernel(float *x, const float *own, ArInbox ib, int rank, int tp, int max_tok, int *state,
-                              const float *gain, TO *out, int hidden, float eps) {
+                              const float *gain, TO *out, int hidden, float eps, SKView skv) {
   pdl_trigger();
   __shared__ float red[8];
   __shared__ float part;
@@ -224,7 +224,10 @@ __global__ void __launch_bounds__(256)
     if (n >= base + per) continue;
 #pragma unroll
     for (int j = 0; j < V; j += 4) {
-      const float4 f = __ldcs(reinterpret_cast<const float4 *>(own + (size_t)t * row + n + j));
+      // skv.ws: the O/down GEMM was deferred (HX_LINEAR_DEFER_REDUCE): split tiles
+      // are summed here from its partial slots in CTA order (the fix-up's bits)
+      const float4 f = skv.ws ? sk_gather4(skv, own, (long)row, t, n + j)
+                              : __ldcs(reinterpret_cast<const float4 *>(own + (size_t)t * row + n + j));
       p[i][j] = f.x; p[i][j + 1] = f.y; p[i][j + 2] = f.z; p[i][j + 3] = f.w;
     }
     const uint4 w = ArPayload<PL>::pack(p[i]);
@@ -388,10 +391,9 @@ extern "C" int hx_tp_inbox_init(void *inbox, int tp, int max_tok, int hidden, hx
   return hx_tp_inbox_init_ex(inbox, tp, max_tok, hidden, HX_F32, stream);
 }
 
-extern "C" int hx_tp_allreduce_push_residual_rmsnorm_ex(float *x, const float *own_part, void *const *inboxes, int rank,
-                                                        int tp, int max_tok, int *state, const float *gain, void *out,
-                                                        int out_dtype, int n_tok, int hidden, float eps,
-                                                        int payload_dtype, hx_stream_t stream) {
+static int ar_push(float *x, const float *own_part, void *const *inboxes, int rank, int tp, int max_tok, int *state,
+                   const float *gain, void *out, int out_dtype, int n_tok, int hidden, float eps, int payload_dtype,
+                   const SKView &skv, hx_stream_t stream) {
   if (n_tok == 0) return 0;
   const int V = payload_dtype == HX_BF16 ? 8 : 4;
   if (!x || !own_part || !inboxes || !state || tp < 1 || tp > kMaxTP || rank < 0 || rank >= tp ||
@@ -404,7 +406,7 @@ extern "C" int hx_tp_allreduce_push_residual_rmsnorm_ex(float *x, const float *o
   const dim3 grid(n_tok * AR_CL);
 #define HX_AR(TO, PL)                                                                                              \
   return launch_cluster(tp_ar_push_rmsnorm_kernel<TO, PL>, grid, dim3(256), 0, st, AR_CL, x, own_part, ib, rank, tp, \
-                        max_tok, state, gain, (TO *)out, hidden, eps)
+                        max_tok, state, gain, (TO *)out, hidden, eps, skv)
   if (payload_dtype == HX_BF16) {
     if (out_dtype == HX_BF16) HX_AR(__nv_bfloat16, __nv_bfloat16);
     HX_AR(float, __nv_bfloat16);
@@ -412,6 +414,28 @@ extern "C" int hx_tp_allreduce_push_residual_rmsnorm_ex(float *x, const float *o
   if (out_dtype == HX_BF16) HX_AR(__nv_bfloat16, float);
   HX_AR(float, float);
 #undef HX_AR
+}
+
+extern "C" int hx_tp_allreduce_push_residual_rmsnorm_ex(float *x, const float *own_part, void *const *inboxes, int rank,
+                                                        int tp, int max_tok, int *state, const float *gain, void *out,
+                                                        int out_dtype, int n_tok, int hidden, float eps,
+                                                        int payload_dtype, hx_stream_t stream) {
+  return ar_push(x, own_part, inboxes, rank, tp, max_tok, state, gain, out, out_dtype, n_tok, hidden, eps,
+                 payload_dtype, SKView{}, stream);
+}
+
+extern "C" int hx_tp_allreduce_push_residual_rmsnorm_sk(float *x, const float *own_part, const void *gemm_workspace,
+                                                        int k_dim, void *const *inboxes, int rank, int tp, int max_tok,
+                                                        int *state, const float *gain, void *out, int out_dtype,
+                                                        int n_tok, int hidden, float eps, int payload_dtype,
+                                                        hx_stream_t stream) {
+  if (n_tok == 0) return 0;
+  if (!gemm_workspace || k_dim <= 0) return HX_ERR_ARG;
+  SKView skv;
+  const int rc = sk_view_for(n_tok, hidden, k_dim, gemm_workspace, &skv);
+  if (rc) return rc;
+  return ar_push(x, own_part, inboxes, rank, tp, max_tok, state, gain, out, out_dtype, n_tok, hidden, eps,
+                 payload_dtype, skv, stream);
 }
 
 extern "C" int hx_tp_allreduce_push_residual_rmsnorm(float *x, const float *own_part, float *const *inboxes, int rank,

@@ -239,6 +239,7 @@ class RankExecutor:
         # decode QKV GEMM without its split-K fix-up tail: partial tiles are reduced
         # in the attention prologue (bit-identical); HX_DEFER_QKV=0 disables
         self.defer_qkv = self.rope_in_attn and os.environ.get("HX_DEFER_QKV", "1") != "0"
+        self.defer_ar = os.environ.get("HX_DEFER_AR", "1") != "0"   # see _peer_defer
         self.qkv32 = z(batch, self.qkv_n, dt=torch.float32) if self.defer_qkv else None
         # tcgen05 prefill attention (default; HX_PREFILL_TC=0 selects the mma.sync
         # kernel): needs V transposed per (sequence, kv head) -- a prefill-only scratch
@@ -300,11 +301,18 @@ class RankExecutor:
                           self.hq, self.hkv, self.hd, self.max_ctx, self.attn_ws)
         # TP=1 decode: the O/down GEMMs leave split tiles as partials and the
         # residual+norm kernel that consumes them does the reduction
-        self._defer_now = self.defer and not prefill_len
+        self._defer_now = (self.defer or self._peer_defer()) and not prefill_len
         self._decode_now = not prefill_len
         # TP>1 decode: the partial goes straight into this rank's NVLink-visible slot
         self._peer_now = self.par is not None and not prefill_len
         self._linear(lw["wo"], self.attn, self._partial_out(2 * li), n_tok)   # row-parallel partial
+
+    def _peer_defer(self) -> bool:
+        """TP>1 decode over the push all-reduce: the O/down GEMMs leave split
+        tiles as partials and the all-reduce kernel reduces them while it reads
+        the row (bit-identical; HX_DEFER_AR=0 keeps the in-GEMM fix-up)."""
+        return (self.defer_ar and self.par is not None and self.par.mode == "push" and self.k is _ops
+                and self.dtype == torch.bfloat16)
 
     def _l2pf(self, prefill_len) -> dict:
         """GEMMs that follow the NVLink all-reduce (TP>1 decode) prefetch extra
@@ -323,7 +331,11 @@ class RankExecutor:
 
     def _add_norm(self, k_dim, gain, out, n_tok, site):
         if self._peer_now:      # all-reduce over peer memory + residual + RMSNorm, one kernel
-            self.par.allreduce_residual_rmsnorm(self.x, site, gain, out, n_tok, self.cfg.rms_eps)
+            if self._defer_now:  # ... with the split-K reduction of the deferred O/down GEMM
+                self.par.allreduce_residual_rmsnorm(self.x, site, gain, out, n_tok, self.cfg.rms_eps,
+                                                    gemm_ws=self.lin_ws, k_dim=k_dim)
+            else:
+                self.par.allreduce_residual_rmsnorm(self.x, site, gain, out, n_tok, self.cfg.rms_eps)
         elif self._defer_now:   # TP=1: split-K reduction inside the residual+norm kernel
             self.k.splitk_residual_rmsnorm(self.x, self.proj, self.lin_ws, n_tok, k_dim, gain, out,
                                            self.cfg.rms_eps)

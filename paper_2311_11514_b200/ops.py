@@ -53,6 +53,8 @@ _SIGS = {
     "hx_tp_inbox_init_ex": ([_P, _I, _I, _I, _I, _P], _I),
     "hx_tp_allreduce_push_residual_rmsnorm_ex": ([_P, _P, ctypes.POINTER(ctypes.c_void_p), _I, _I, _I, _P, _P, _P,
                                                   _I, _I, _I, _F, _I, _P], _I),
+    "hx_tp_allreduce_push_residual_rmsnorm_sk": ([_P, _P, _P, _I, ctypes.POINTER(ctypes.c_void_p), _I, _I, _I, _P,
+                                                  _P, _P, _I, _I, _I, _F, _I, _P], _I),
     "hx_handoff_inbox_bytes": ([_SZ], _SZ),
     "hx_handoff_inbox_init": ([_P, _SZ, _P], _I),
     "hx_handoff_push": ([_P, ctypes.POINTER(ctypes.c_void_p), _I, _SZ, _SZ, _P, _P], _I),
@@ -426,8 +428,19 @@ class PeerAllReduce:
         ptr = self.peer[f"slot{site % 2}"][self.rank]
         return _tensor_at(ptr, (self.max_tok, self.hidden))
 
-    def allreduce_residual_rmsnorm(self, x, site, gain, out, n_tok, eps):
+    def allreduce_residual_rmsnorm(self, x, site, gain, out, n_tok, eps, gemm_ws=None, k_dim=0):
+        """gemm_ws / k_dim: the slot was written by a deferred GEMM
+        (linear(..., defer_reduce=True) with that workspace); push mode only."""
         lib = load()
+        if gemm_ws is not None:
+            if self.mode != "push":
+                raise ValueError("deferred split-K all-reduce needs mode='push'")
+            _check(lib.hx_tp_allreduce_push_residual_rmsnorm_sk(
+                _p(x), self.peer[f"slot{site % 2}"][self.rank], _p(gemm_ws), k_dim, self._arr["inbox"], self.rank,
+                self.tp, self.max_tok, _p(self.site_state), _p(gain), _p(out),
+                dtype_code(out.dtype) if out is not None else HX_F32, n_tok, self.hidden, eps, self._pl, _stream()),
+                "hx_tp_allreduce_push_residual_rmsnorm_sk")
+            return
         if self.mode == "push":
             _check(lib.hx_tp_allreduce_push_residual_rmsnorm_ex(
                 _p(x), self.peer[f"slot{site % 2}"][self.rank], self._arr["inbox"], self.rank, self.tp, self.max_tok,

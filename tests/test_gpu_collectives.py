@@ -133,6 +133,55 @@ def test_peer_allreduce_single_gpu_streams(tp, n_tok, hidden, out_dtype):
             assert torch.equal(results[mode][0][r], x_ref), f"{mode}: residual != rank-order fp32 sum (rank {r})"
 
 
+@pytest.mark.parametrize("tp", [2, 4])
+@pytest.mark.parametrize("n_tok,hidden,k_dim", [(8, 8192, 2048), (16, 8192, 7168), (5, 4096, 11008)])
+def test_peer_allreduce_deferred_gemm_single_gpu(tp, n_tok, hidden, k_dim):
+    """TP>1 decode with the row-parallel GEMM deferred (HX_LINEAR_DEFER_REDUCE):
+    each rank's all-reduce sums the GEMM's split tiles from its partial slots
+    while reading the row (hx_tp_allreduce_push_residual_rmsnorm_sk). Residual
+    and output must be BITWISE those of the GEMM with its in-kernel fix-up
+    followed by the plain push all-reduce, over consecutive calls."""
+    n_tok = min(n_tok, ops.PEER_AR_CORESIDENT // (4 * tp))
+    eps, calls = 1e-5, 3
+    g = torch.Generator(device=DEV).manual_seed(tp * 7 + n_tok + k_dim)
+    x0 = torch.randn(n_tok, hidden, device=DEV, generator=g)
+    gain = 1 + 0.02 * torch.randn(hidden, device=DEV, generator=g)
+    ws_words = ops.linear_workspace(torch.bfloat16, n_tok, hidden, k_dim) // 4 + 64
+    ws = [torch.zeros(ws_words, dtype=torch.int32, device=DEV) for _ in range(tp)]
+    calls_in = []
+    for c in range(calls):
+        w = [ops.PackedWeight((torch.randn(hidden, k_dim, device=DEV, generator=g) * 0.02).bfloat16())
+             for _ in range(tp)]
+        a = [torch.randn(n_tok, k_dim, device=DEV, generator=g).bfloat16() for _ in range(tp)]
+        calls_in.append((w, a))
+    results = {}
+    for deferred in (False, True):
+        group = ops.PeerAllReduce.local_group(tp, 32, hidden, 4, mode="push", payload="bf16")
+        xs = [x0.clone() for _ in range(tp)]
+        streams = [torch.cuda.Stream() for _ in range(tp)]
+        outs = []
+        for c, (w, a) in enumerate(calls_in):
+            site = c % 4
+            for r in range(tp):   # every rank's GEMM first (own workspace), then the all-reduces together
+                ops.linear(w[r], a[r], group[r].slot(site), n_tok, ws[r], defer_reduce=deferred)
+            torch.cuda.synchronize()
+            o = [torch.empty(n_tok, hidden, device=DEV, dtype=torch.bfloat16) for _ in range(tp)]
+            for r in range(tp):
+                with torch.cuda.stream(streams[r]):
+                    kw = {"gemm_ws": ws[r], "k_dim": k_dim} if deferred else {}
+                    group[r].allreduce_residual_rmsnorm(xs[r], site, gain, o[r], n_tok, eps, **kw)
+            torch.cuda.synchronize()
+            outs.append(o)
+        for q in group:
+            q.close()
+        results[deferred] = (xs, outs)
+    for r in range(tp):
+        assert torch.equal(results[True][0][r], results[False][0][r]), f"residual differs (rank {r})"
+        assert torch.equal(results[True][0][r], results[True][0][0])
+        for c in range(calls):
+            assert torch.equal(results[True][1][c][r], results[False][1][c][r]), f"output differs (call {c})"
+
+
 def test_peer_allreduce_graph_replay_single_gpu():
     """The emulated ranks' all-reduces captured in one CUDA graph (fork/join
     over per-rank streams) and replayed: the call counters and re-armed

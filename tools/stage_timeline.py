@@ -1,18 +1,13 @@
-"""Per-stage attribution of the multi-GPU decode step (torchrun, one rank per GPU).
+"""Per-CTA timeline of one TP stage's decode step on real ranks (torchrun):
+rank 0 records its stream-K GEMMs and decode attention (hx_debug_trace) in the
+engine's own decode graph, so the NVLink all-reduces sit between the GEMMs as
+in the bench. Prints, per GEMM role, the wait after the previous traced kernel,
+the run after the wait and the tail, plus the QKV -> attention -> O phases.
 
-    torchrun --nproc-per-node 4 --master-addr 127.0.0.1 tools/stage_timeline.py \
-        --model llama2-70b --plan 2,1,1 --layers 40,20,20
-
-After a warm generate, every rank:
-  1. replays its own stage's decode graph back to back (stage-mates start
-     together after a barrier; other stages idle) -> pure stage compute time;
-  2. runs real decode steps with CUDA events around its phases
-     (ids return, hidden recv, graph replay, hidden send) -> where a step waits.
-Prints one line per rank.
+    torchrun --nproc-per-node 4 --master-addr 127.0.0.1 tools/stage_timeline.py --tp 4 --layers 20
 """
 import argparse
 import os
-import statistics
 import sys
 from pathlib import Path
 
@@ -21,82 +16,83 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
+from paper_2311_11514_b200 import ops
 from paper_2311_11514_b200.config import preset
 from paper_2311_11514_b200.engine import Engine
 from paper_2311_11514_b200.plan import simple_plan
 
-
-def main():
-    os.environ.setdefault("HX_P2P", "0")  # solo stage replays cannot wait on P2P hand-offs
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--model", default="llama2-70b")
-    ap.add_argument("--plan", default="2,1,1")
-    ap.add_argument("--layers", default="40,20,20")
-    ap.add_argument("--batch", type=int, default=32)
-    ap.add_argument("--s-in", type=int, default=1024)
-    ap.add_argument("--s-out", type=int, default=64)
-    a = ap.parse_args()
-    rank, local = int(os.environ["RANK"]), int(os.environ["LOCAL_RANK"])
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+ap = argparse.ArgumentParser()
+ap.add_argument("--model", default="llama2-70b")
+ap.add_argument("--tp", type=int, default=4)
+ap.add_argument("--layers", type=int, default=20)
+ap.add_argument("--batch", type=int, default=32)
+ap.add_argument("--s-in", type=int, default=1024)
+a = ap.parse_args()
+local = int(os.environ.get("LOCAL_RANK", "0"))
+torch.cuda.set_device(local)
+dev = torch.device("cuda", local)
+if a.tp > 1:
     dist.init_process_group("nccl", device_id=dev)
-    cfg = preset(a.model)
-    plan = simple_plan([int(x) for x in a.plan.split(",")], [int(x) for x in a.layers.split(",")])
-    eng = Engine(plan, cfg, dtype="bf16", batch=a.batch, max_prompt=a.s_in, max_out=a.s_out, comm="dist",
-                 device=dev, weights="device")
-    prompt = np.random.default_rng(1).integers(0, cfg.vocab, size=(a.batch, a.s_in), dtype=np.int32)
-    r = eng.generate(prompt, a.s_out)
-    r = eng.generate(prompt, a.s_out)
-    step_p50 = statistics.median(r.step_ms)
-    d = eng.drivers[0]
-    g = eng._graphs[0]
-    # 1. solo replays, stage by stage (the other stages wait at the barrier)
-    solo = {}
-    for j in range(eng.num_stages):
-        dist.barrier()
-        torch.cuda.synchronize()
-        if d.stage == j:
-            if d.tp > 1:
-                dist.barrier(group=eng.comm.groups[d.role.tp_group])
-            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            g.replay()
-            s0.record()
-            for _ in range(10):
-                g.replay()
-            s1.record()
-            torch.cuda.synchronize()
-            solo[j] = s0.elapsed_time(s1) / 10
+rank = dist.get_rank() if a.tp > 1 else 0
+cfg = preset(a.model, num_layers=a.layers)
+eng = Engine(simple_plan([a.tp], [a.layers]), cfg, dtype="bf16", batch=a.batch, max_prompt=a.s_in, max_out=8,
+             comm="dist" if a.tp > 1 else "local", device=dev, weights="device")
+prompt = np.random.default_rng(1).integers(0, cfg.vocab, size=(a.batch, a.s_in), dtype=np.int32)
+eng.generate(prompt, 8)
+lib = ops.load()
+cap = 400 * 1024
+buf = torch.zeros(cap * 8, dtype=torch.int64, device=dev)
+if rank == 0:
+    lib.hx_debug_trace(buf.data_ptr(), cap)
+eng._graph_cache.clear()           # recapture with the trace armed (rank 0)
+eng.generate(prompt, 8)
+used = lib.hx_debug_trace(None, 0) if rank == 0 else 0
+torch.cuda.synchronize()
+if rank == 0:
+    tr = buf.view(-1, 8)[:used].cpu().numpy().astype(np.int64)
+    is_attn = (tr[:, 3] >> 40) & 1
+    launches, i = [], 0
+    while i < used:
+        if is_attn[i]:
+            j = i
+            while j < used and is_attn[j]:
+                j += 1
+            launches.append(("attn", tr[i:j]))
+            i = j
+        else:
+            launches.append(("gemm", tr[i:i + 148]))
+            i += 148
+    # anchor on the attention launches: QKV before, O, gate/up, down after
+    names = ["qkv", "attn", "o", "gu", "down"]
+    stats = {n: [] for n in names}
+    att_idx = [k for k, (kind, _) in enumerate(launches) if kind == "attn"]
+    for k in att_idx:
+        if k < 2 or k + 3 >= len(launches):
+            continue
+        seq = launches[k - 2:k + 4]   # previous layer's down, qkv, attn, o, gu, down
+        st = [r[:, 0].min() for _, r in seq]
+        if any(st[j + 1] < st[j] or st[j + 1] - st[j] > 1_000_000 for j in range(len(st) - 1)):
+            continue                  # slots of an eager launch (stale) or a step boundary
+        for j, nm in enumerate(names):
+            kind, r = seq[j + 1]
+            prev_end = seq[j][1][:, 2].max()
+            if kind == "gemm":
+                stats[nm].append(((r[:, 1].min() - prev_end) / 1e3, (r[:, 2].max() - r[:, 1].min()) / 1e3,
+                                  (r[:, 2].max() - np.median(r[:, 2])) / 1e3))
+            else:
+                stats[nm].append(((np.median(r[:, 4]) - prev_end) / 1e3, (r[:, 2][r[:, 2] > 0].max() - prev_end) / 1e3, 0.0))
+        stats.setdefault("layer", []).append((seq[-1][1][:, 2].max() - seq[0][1][:, 2].max()) / 1e3)
+    n = len(stats["qkv"])
+    med = lambda v, c: float(np.median(v[:, c]))
+    print(f"{a.model} TP={a.tp} x {a.layers} layers, b={a.batch}, ctx {a.s_in}: rank 0, {n} layers of one decode step (us)")
+    for nm in names:
+        v = np.array(stats[nm])
+        if nm == "attn":
+            print(f"  attention: q ready {med(v, 0):6.2f}  end {med(v, 1):6.2f} after the QKV GEMM's end")
+        else:
+            print(f"  {nm:5s}: wait after previous traced kernel {med(v, 0):6.2f}  run after wait "
+                  f"{med(v, 1):6.2f}  tail {med(v, 2):5.2f}")
+    print(f"  per layer (previous down end -> down end): median {np.median(stats['layer']):.1f} us  (medians over layers)")
+if a.tp > 1:
     dist.barrier()
-    torch.cuda.synchronize()
-    # 2. real steps with phase events (prefill first so the KV state is valid)
-    eng._reset(a.batch, a.s_in, a.s_out)
-    for e in eng.execs:
-        if e.role.is_first:
-            e.prompt[:a.batch * a.s_in].copy_(torch.from_numpy(prompt.reshape(-1)))
-    eng._prefill(a.batch, a.s_in)
-    ph = {"ids": [], "recv": [], "graph": [], "send": []}
-    for _ in range(1, a.s_out):
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
-        evs[0].record()
-        eng._return_ids()
-        evs[1].record()
-        if d.stage > 0:
-            d.recv_hidden(a.batch)
-        evs[2].record()
-        g.replay()
-        evs[3].record()
-        if d.stage < eng.num_stages - 1:
-            d.send_hidden(a.batch)
-        evs[4].record()
-        torch.cuda.synchronize()
-        for k, (x, y) in zip(ph, zip(evs, evs[1:])):
-            ph[k].append(x.elapsed_time(y))
-    med = {k: round(statistics.median(v), 3) for k, v in ph.items()}
-    print(f"rank {rank} stage {d.stage} tp {d.tp}: generate p50 step {step_p50:.3f} ms | solo graph "
-          f"{solo.get(d.stage, float('nan')):.3f} ms | in-step phases (ms) {med}", flush=True)
-    dist.barrier()
-    os._exit(0)
-
-
-if __name__ == "__main__":
-    main()
+os._exit(0)
