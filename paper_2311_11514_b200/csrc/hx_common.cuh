@@ -413,6 +413,49 @@ __device__ __forceinline__ SkTile sk_tile(const SKView &v, int tt) {
   return t;
 }
 
+// NQ float4 gathers at once (features n[q]..n[q]+3 of token t): the tiles'
+// contributor ranges ti[q] are computed by the caller (before its dependency
+// wait -- they are GEMM geometry, not data) and every item's contributor loads
+// are in flight together; per item the sum is sk_gather4's (CTA order from 0).
+template <int NQ>
+__device__ __forceinline__ void sk_gather_n(const SKView &v, const SkTile (&ti)[NQ], const float *y, long ldy, int t,
+                                            const int (&n)[NQ], const bool (&act)[NQ], float4 (&out)[NQ]) {
+  constexpr int MAXC = 8;
+  int cl[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    out[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    cl[q] = -1;
+    if (act[q]) {
+      if (ti[q].whole()) out[q] = *reinterpret_cast<const float4 *>(y + (long)t * ldy + n[q]);
+      else cl[q] = ti[q].c_last;
+    }
+  }
+  for (int base = 0;; base += MAXC) {
+    float4 f[NQ][MAXC];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+#pragma unroll
+      for (int k = 0; k < MAXC; ++k) {
+        const int cc = ti[q].c_first + base + k;
+        if (cc <= cl[q])
+          f[q][k] = __ldcg(reinterpret_cast<const float4 *>(v.ws + ((size_t)ti[q].slot(cc) * v.BN + t) * kSkRows +
+                                                            n[q] % kSkRows));
+      }
+    bool more = false;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+#pragma unroll
+      for (int k = 0; k < MAXC; ++k)
+        if (ti[q].c_first + base + k <= cl[q]) {
+          out[q].x += f[q][k].x; out[q].y += f[q][k].y; out[q].z += f[q][k].z; out[q].w += f[q][k].w;
+        }
+      more |= ti[q].c_first + base + MAXC <= cl[q];
+    }
+    if (!more) break;
+  }
+}
+
 __device__ __forceinline__ float4 sk_gather4(const SKView &v, const float *y, long ldy, int t, int n) {
   const int tt = n / kSkRows, r = n % kSkRows;
   const SkTile ti = sk_tile(v, tt);

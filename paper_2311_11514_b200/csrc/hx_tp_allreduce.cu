@@ -208,15 +208,38 @@ __global__ void __launch_bounds__(256)
   const size_t row = (size_t)hidden;
   if (out && threadIdx.x < per / 32)   // the gain is a weight: pull this CTA's slice into L1 before the wait
     asm volatile("prefetch.global.L1 [%0];" ::"l"(gain + base + threadIdx.x * 32));
+  constexpr int V = ArPayload<PL>::V;   // features per 16-byte vector
+  constexpr int NV = 2048 / (256 * V);  // vectors per thread: <= 2048 features per CTA (hidden <= 8192)
+  constexpr int NQ = NV * V / 4;        // float4 reads of this rank's partial per thread
+  // deferred GEMM (skv.ws): the contributor ranges of this thread's tiles, before the wait
+  SkTile sti[NQ];
+  int sn[NQ];
+  bool sact[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    sn[q] = base + ((q / (V / 4)) * 256 + threadIdx.x) * V + (q % (V / 4)) * 4;
+    sact[q] = sn[q] < base + per;
+    sti[q] = SkTile{0, -1, 0};
+    if (skv.ws && sact[q]) sti[q] = sk_tile(skv, sn[q] / kSkRows);
+  }
   pdl_wait();  // this rank's partial (previous kernel) is complete
   const int call = *(volatile int *)(state + blockIdx.x);
   const int buf = call & 1;
   // inbox element index of (buffer, sender r, token t, feature n); payload elements of PL
-  constexpr int V = ArPayload<PL>::V;   // features per 16-byte vector
-  constexpr int NV = 2048 / (256 * V);  // vectors per thread: <= 2048 features per CTA (hidden <= 8192)
   PL *mine = reinterpret_cast<PL *>(ib.box[rank]);
   auto at = [&](PL *box, int r, int n) { return box + (((size_t)buf * tp + r) * max_tok + t) * row + n; };
   float p[NV][V];
+  // this rank's partial: plain, or (skv.ws: the O/down GEMM was deferred,
+  // HX_LINEAR_DEFER_REDUCE) its split tiles summed from the partial slots in CTA
+  // order -- the fix-up's bits -- every load of the thread in flight together
+  float4 f4[NQ];
+  if (skv.ws) {
+    sk_gather_n<NQ>(skv, sti, own, (long)row, t, sn, sact, f4);
+  } else {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+      if (sact[q]) f4[q] = __ldcs(reinterpret_cast<const float4 *>(own + (size_t)t * row + sn[q]));
+  }
   // 1. push my partial slice of row t to every peer (remote stores, fire and forget)
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
@@ -224,10 +247,7 @@ __global__ void __launch_bounds__(256)
     if (n >= base + per) continue;
 #pragma unroll
     for (int j = 0; j < V; j += 4) {
-      // skv.ws: the O/down GEMM was deferred (HX_LINEAR_DEFER_REDUCE): split tiles
-      // are summed here from its partial slots in CTA order (the fix-up's bits)
-      const float4 f = skv.ws ? sk_gather4(skv, own, (long)row, t, n + j)
-                              : __ldcs(reinterpret_cast<const float4 *>(own + (size_t)t * row + n + j));
+      const float4 f = f4[i * (V / 4) + j / 4];
       p[i][j] = f.x; p[i][j + 1] = f.y; p[i][j + 2] = f.z; p[i][j + 3] = f.w;
     }
     const uint4 w = ArPayload<PL>::pack(p[i]);

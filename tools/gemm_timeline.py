@@ -62,6 +62,8 @@ for _ in range(3):
     g.replay()
 torch.cuda.synchronize()
 tr = buf.view(-1, 8)[:used].cpu().numpy().astype(np.int64)
+tr = tr[((tr[:, 3] >> 40) & 1) == 0]   # drop the decode attention's records (same trace)
+used = len(tr)
 G = 148
 n = used // G
 names = ["qkv", "o", "gu", "down"]
