@@ -426,6 +426,7 @@ struct SKArgs {
   int *counters;
   unsigned long long *trace;  // optional per-CTA timeline (hx_debug_trace): start, wait done, end, smid
   int l2pf;                   // weight tiles beyond the smem ring prefetched into L2 before the PDL wait
+  int prewait;                // ring stages whose weight tiles are requested before the PDL wait
   const uint8_t *w_ptr;       // packed weights (for the epilogue warps' L2 prefetch)
 };
 
@@ -496,13 +497,19 @@ __global__ void __launch_bounds__(192, 2)
       auto load_x = [&](int s, int u) { tma_load_2d(sb + s * B_BYTES, &tm_x, &full[s], (u % p.KB) * BK, 0, pol_x); };
       const int n = u1 - u0;
       const int pre = min(n, STAGES);
-      for (int i = 0; i < pre; ++i) {  // weights first: they do not depend on the previous kernel
+      const int pw = min(pre, p.prewait);
+      for (int i = 0; i < pw; ++i) {  // weights first: they do not depend on the previous kernel
         mbar_arrive_expect_tx(&full[i], A_BYTES + B_BYTES);
         load_w(i, u0 + i);
       }
       pdl_wait();
       if (p.trace) p.trace[8 * c + 1] = globaltimer();
-      for (int i = 0; i < pre; ++i) load_x(i, u0 + i);
+      for (int i = 0; i < pw; ++i) load_x(i, u0 + i);
+      for (int i = pw; i < pre; ++i) {
+        mbar_arrive_expect_tx(&full[i], A_BYTES + B_BYTES);
+        load_w(i, u0 + i);
+        load_x(i, u0 + i);
+      }
       for (int i = pre; i < n; ++i) {
         const int s = i % STAGES;
         mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
@@ -1096,6 +1103,11 @@ extern "C" int hx_linear(const void *w, const void *x, void *y, int dtype, int y
     sk.counters = reinterpret_cast<int *>(workspace);
     sk.ws = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(workspace) + kTicketBytes);
     const size_t g = (size_t)sk_grid(sk.units);
+    static const int prewait = [] {  // HX_SK_PREWAIT: ring stages streamed before the PDL wait (tuning)
+      const char *e = getenv("HX_SK_PREWAIT");
+      return e ? atoi(e) : 64;
+    }();
+    sk.prewait = prewait;
     if (g_trace && g_trace_pos + g <= g_trace_cap) {
       sk.trace = g_trace + 8 * g_trace_pos;
       g_trace_pos += g;

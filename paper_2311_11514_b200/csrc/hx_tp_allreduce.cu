@@ -23,6 +23,8 @@
 
 namespace hx {
 
+unsigned long long *hx_trace_slots(size_t n);  // hx_gemm.cu (hx_debug_trace)
+
 constexpr int kMaxTP = 8;
 
 struct ArPeers {
@@ -198,14 +200,26 @@ struct ArPayload<__nv_bfloat16> {
 template <typename TO, typename PL>
 __global__ void __launch_bounds__(256)
     tp_ar_push_rmsnorm_kernel(float *x, const float *own, ArInbox ib, int rank, int tp, int max_tok, int *state,
-                              const float *gain, TO *out, int hidden, float eps, SKView skv) {
+                              const float *gain, TO *out, int hidden, float eps, SKView skv,
+                              unsigned long long *trace) {
   pdl_trigger();
+  // hx_debug_trace: start, wait done, end, smid | 1 << 41, partial read, pushed, peers arrived, summed
+  unsigned long long *tr = trace ? trace + 8 * blockIdx.x : nullptr;
+  auto stamp = [&](int f) {
+    if (tr && threadIdx.x == 0) {
+      unsigned long long tt;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tt));
+      tr[f] = tt;
+    }
+  };
+  stamp(0);
   __shared__ float red[8];
-  __shared__ float part;
+  __shared__ float parts[AR_CL];
   const unsigned cr = cluster_rank();
   const int t = blockIdx.x / AR_CL;
   const int per = hidden / AR_CL, base = (int)cr * per;
   const size_t row = (size_t)hidden;
+  if (out) cluster_arrive_relaxed();  // matched by the wait before the first DSMEM store (every CTA started)
   if (out && threadIdx.x < per / 32)   // the gain is a weight: pull this CTA's slice into L1 before the wait
     asm volatile("prefetch.global.L1 [%0];" ::"l"(gain + base + threadIdx.x * 32));
   constexpr int V = ArPayload<PL>::V;   // features per 16-byte vector
@@ -223,6 +237,12 @@ __global__ void __launch_bounds__(256)
     if (skv.ws && sact[q]) sti[q] = sk_tile(skv, sn[q] / kSkRows);
   }
   pdl_wait();  // this rank's partial (previous kernel) is complete
+  stamp(1);
+  if (tr && threadIdx.x == 0) {
+    unsigned sm;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(sm));
+    tr[3] = sm | (1ull << 41);
+  }
   const int call = *(volatile int *)(state + blockIdx.x);
   const int buf = call & 1;
   // inbox element index of (buffer, sender r, token t, feature n); payload elements of PL
@@ -232,7 +252,10 @@ __global__ void __launch_bounds__(256)
   // this rank's partial: plain, or (skv.ws: the O/down GEMM was deferred,
   // HX_LINEAR_DEFER_REDUCE) its split tiles summed from the partial slots in CTA
   // order -- the fix-up's bits -- every load of the thread in flight together
-  float4 f4[NQ];
+  float4 f4[NQ], x4[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q)  // the residual row too: its loads overlap the push and the poll
+    if (sact[q]) x4[q] = *reinterpret_cast<const float4 *>(x + (size_t)t * row + sn[q]);
   if (skv.ws) {
     sk_gather_n<NQ>(skv, sti, own, (long)row, t, sn, sact, f4);
   } else {
@@ -240,6 +263,7 @@ __global__ void __launch_bounds__(256)
     for (int q = 0; q < NQ; ++q)
       if (sact[q]) f4[q] = __ldcs(reinterpret_cast<const float4 *>(own + (size_t)t * row + sn[q]));
   }
+  stamp(4);
   // 1. push my partial slice of row t to every peer (remote stores, fire and forget)
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
@@ -255,6 +279,7 @@ __global__ void __launch_bounds__(256)
     for (int r = 0; r < tp; ++r)
       if (r != rank) *reinterpret_cast<uint4 *>(at(reinterpret_cast<PL *>(ib.box[r]), rank, n)) = w;
   }
+  stamp(5);
   // 2. poll my inbox for every peer's slice, re-arm it in place, sum in rank order
   //    (bitwise identical on all ranks), residual
   const uint4 s4 = ArPayload<PL>::sentinel();
@@ -287,27 +312,28 @@ __global__ void __launch_bounds__(256)
     }
 #pragma unroll
     for (int j = 0; j < V; j += 4) {
-      float4 acc = *reinterpret_cast<const float4 *>(x + (size_t)t * row + n + j);
+      float4 acc = x4[i * (V / 4) + j / 4];
       acc.x += sum[j]; acc.y += sum[j + 1]; acc.z += sum[j + 2]; acc.w += sum[j + 3];
       *reinterpret_cast<float4 *>(x + (size_t)t * row + n + j) = acc;
       v[i][j] = acc.x; v[i][j + 1] = acc.y; v[i][j + 2] = acc.z; v[i][j + 3] = acc.w;
       ss += acc.x * acc.x + acc.y * acc.y + acc.z * acc.z + acc.w * acc.w;
     }
   }
+  stamp(6);
   // 3. RMSNorm across the cluster (DSMEM), same summation order in every CTA
   if (out) {
     ss = warp_sum(ss);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
     __syncthreads();
-    if (threadIdx.x == 0) {
+    cluster_wait();
+    if (threadIdx.x == 0) {  // this CTA's sum of squares into every cluster CTA's parts[rank]
       float s2 = 0.f;
       for (int i = 0; i < 8; ++i) s2 += red[i];
-      part = s2;
+      for (int c = 0; c < AR_CL; ++c) dsmem_st_f32(&parts[cr], c, s2);
     }
-    cluster_sync_all();
+    cluster_sync_all();  // every CTA's stores into this CTA's parts[] are visible; no remote reads follow
     float tot = 0.f;
-    for (int c = 0; c < AR_CL; ++c) tot += dsmem_ld_f32(&part, c);
-    cluster_sync_all();  // peers have read `part` before this CTA may exit
+    for (int c = 0; c < AR_CL; ++c) tot += parts[c];   // same order in every CTA
     const float inv = 1.0f / sqrtf(tot / (float)hidden + eps);
     TO *o = out + (size_t)t * row;
 #pragma unroll
@@ -324,6 +350,7 @@ __global__ void __launch_bounds__(256)
   }
   __syncthreads();  // every thread has read `call`
   if (threadIdx.x == 0) *(volatile int *)(state + blockIdx.x) = call + 1;
+  stamp(2);
 }
 
 __global__ void fill_u32_kernel(uint32_t *p, size_t n, uint32_t v) {
@@ -424,9 +451,10 @@ static int ar_push(float *x, const float *own_part, void *const *inboxes, int ra
   for (int r = 0; r < tp; ++r) ib.box[r] = reinterpret_cast<float *>(inboxes[r]);
   cudaStream_t st = as_stream(stream);
   const dim3 grid(n_tok * AR_CL);
+  unsigned long long *tr = hx_trace_slots((size_t)grid.x);
 #define HX_AR(TO, PL)                                                                                              \
   return launch_cluster(tp_ar_push_rmsnorm_kernel<TO, PL>, grid, dim3(256), 0, st, AR_CL, x, own_part, ib, rank, tp, \
-                        max_tok, state, gain, (TO *)out, hidden, eps, skv)
+                        max_tok, state, gain, (TO *)out, hidden, eps, skv, tr)
   if (payload_dtype == HX_BF16) {
     if (out_dtype == HX_BF16) HX_AR(__nv_bfloat16, __nv_bfloat16);
     HX_AR(float, __nv_bfloat16);

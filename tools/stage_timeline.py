@@ -50,38 +50,48 @@ used = lib.hx_debug_trace(None, 0) if rank == 0 else 0
 torch.cuda.synchronize()
 if rank == 0:
     tr = buf.view(-1, 8)[:used].cpu().numpy().astype(np.int64)
-    is_attn = (tr[:, 3] >> 40) & 1
+    kind_of = np.where((tr[:, 3] >> 40) & 1, 1, np.where((tr[:, 3] >> 41) & 1, 2, 0))  # 0 GEMM, 1 attn, 2 AR
     launches, i = [], 0
     while i < used:
-        if is_attn[i]:
+        if kind_of[i]:
             j = i
-            while j < used and is_attn[j]:
+            while j < used and kind_of[j] == kind_of[i]:
                 j += 1
-            launches.append(("attn", tr[i:j]))
+            launches.append(("attn" if kind_of[i] == 1 else "ar", tr[i:j]))
             i = j
         else:
             launches.append(("gemm", tr[i:i + 148]))
             i += 148
-    # anchor on the attention launches: QKV before, O, gate/up, down after
-    names = ["qkv", "attn", "o", "gu", "down"]
+    has_ar = any(k == "ar" for k, _ in launches)
+    # anchor on the attention launches: [prev AR,] QKV, attention, O, [AR,] gate/up, down[, AR]
+    names = ["qkv", "attn", "o", "ar1", "gu", "down", "ar2"] if has_ar else ["qkv", "attn", "o", "gu", "down"]
+    lead = 2 if has_ar else 2
     stats = {n: [] for n in names}
+    layer = []
     att_idx = [k for k, (kind, _) in enumerate(launches) if kind == "attn"]
     for k in att_idx:
-        if k < 2 or k + 3 >= len(launches):
+        if k < lead or k - 1 + len(names) > len(launches):
             continue
-        seq = launches[k - 2:k + 4]   # previous layer's down, qkv, attn, o, gu, down
+        seq = launches[k - lead:k - 1 + len(names)]   # the previous layer's last launch, then this layer's
         st = [r[:, 0].min() for _, r in seq]
         if any(st[j + 1] < st[j] or st[j + 1] - st[j] > 1_000_000 for j in range(len(st) - 1)):
             continue                  # slots of an eager launch (stale) or a step boundary
+        if [kd for kd, _ in seq[1:]] != [("attn" if n == "attn" else "ar" if n.startswith("ar") else "gemm")
+                                         for n in names]:
+            continue
         for j, nm in enumerate(names):
             kind, r = seq[j + 1]
             prev_end = seq[j][1][:, 2].max()
+            us = lambda v: (v - prev_end) / 1e3
             if kind == "gemm":
-                stats[nm].append(((r[:, 1].min() - prev_end) / 1e3, (r[:, 2].max() - r[:, 1].min()) / 1e3,
+                stats[nm].append((us(r[:, 1].min()), (r[:, 2].max() - r[:, 1].min()) / 1e3,
                                   (r[:, 2].max() - np.median(r[:, 2])) / 1e3))
-            else:
-                stats[nm].append(((np.median(r[:, 4]) - prev_end) / 1e3, (r[:, 2][r[:, 2] > 0].max() - prev_end) / 1e3, 0.0))
-        stats.setdefault("layer", []).append((seq[-1][1][:, 2].max() - seq[0][1][:, 2].max()) / 1e3)
+            elif kind == "attn":
+                stats[nm].append((us(np.median(r[:, 4])), us(r[:, 2][r[:, 2] > 0].max()), 0.0))
+            else:   # all-reduce: wait done, partial read, pushed, peers arrived, end (max over CTAs)
+                stats[nm].append((us(r[:, 1].max()), us(r[:, 4].max()), us(r[:, 5].max()), us(np.median(r[:, 6])),
+                                  us(r[:, 6].max()), us(r[:, 2].max())))
+        layer.append((seq[-1][1][:, 2].max() - seq[0][1][:, 2].max()) / 1e3)
     n = len(stats["qkv"])
     med = lambda v, c: float(np.median(v[:, c]))
     print(f"{a.model} TP={a.tp} x {a.layers} layers, b={a.batch}, ctx {a.s_in}: rank 0, {n} layers of one decode step (us)")
@@ -89,10 +99,13 @@ if rank == 0:
         v = np.array(stats[nm])
         if nm == "attn":
             print(f"  attention: q ready {med(v, 0):6.2f}  end {med(v, 1):6.2f} after the QKV GEMM's end")
+        elif nm.startswith("ar"):
+            print(f"  {nm:5s}: after the previous GEMM's end: wait done {med(v, 0):6.2f}  partial read {med(v, 1):6.2f}  "
+                  f"pushed {med(v, 2):6.2f}  peers arrived med/max {med(v, 3):6.2f}/{med(v, 4):6.2f}  end {med(v, 5):6.2f}")
         else:
             print(f"  {nm:5s}: wait after previous traced kernel {med(v, 0):6.2f}  run after wait "
                   f"{med(v, 1):6.2f}  tail {med(v, 2):5.2f}")
-    print(f"  per layer (previous down end -> down end): median {np.median(stats['layer']):.1f} us  (medians over layers)")
+    print(f"  per layer: median {np.median(layer):.1f} us  (medians over layers)")
 if a.tp > 1:
     dist.barrier()
 os._exit(0)
