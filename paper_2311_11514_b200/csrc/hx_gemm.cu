@@ -669,11 +669,12 @@ __global__ void __launch_bounds__(256)
   // RMS sum of squares is combined across the cluster through DSMEM
   pdl_trigger();
   __shared__ float red[8];
-  __shared__ float part;
+  __shared__ float parts[SK_CL];
   const unsigned cr = cluster_rank();
   const int t = blockIdx.x / SK_CL;
   const int per = hidden / SK_CL, base = (int)cr * per;
   float *xr = x + (size_t)t * hidden;
+  if (out) cluster_arrive_relaxed();  // matched by the wait before the first DSMEM store (every CTA started)
   constexpr int MAXV = 2;  // hidden <= SK_CL * 2 * 4 * 256 = 8192
   float4 xv[MAXV], dv[MAXV], gv[MAXV];
   // the gain is a weight: fetch it before waiting on the producer GEMM
@@ -706,15 +707,15 @@ __global__ void __launch_bounds__(256)
   ss = warp_sum(ss);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
   __syncthreads();
-  if (threadIdx.x == 0) {
+  cluster_wait();
+  if (threadIdx.x == 0) {  // this CTA's sum of squares into every cluster CTA's parts[rank]
     float s = 0.f;
     for (int i = 0; i < 8; ++i) s += red[i];
-    part = s;
+    for (int c = 0; c < SK_CL; ++c) dsmem_st_f32(&parts[cr], c, s);
   }
-  cluster_sync_all();
+  cluster_sync_all();  // every CTA's stores into this CTA's parts[] are visible; no remote reads follow
   float tot = 0.f;
-  for (int c = 0; c < SK_CL; ++c) tot += dsmem_ld_f32(&part, c);  // same order in every CTA
-  cluster_sync_all();  // peers have read `part` before this CTA may exit
+  for (int c = 0; c < SK_CL; ++c) tot += parts[c];  // same order in every CTA
   const float inv = 1.0f / sqrtf(tot / (float)hidden + eps);
   TO *o = out + (size_t)t * hidden;
 #pragma unroll
